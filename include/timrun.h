@@ -1,0 +1,168 @@
+/*
+ * timrun.h — C ABI of libtimrun.so, the B200 (sm_100a) working-memory decode path.
+ *
+ * This is the drop-in boundary for the reference runtime `threadrun`
+ * (/root/reference/pkg/src/threadrun).  The reference's plugin interface for
+ * this path is the duck-typed model-backend protocol consumed by `Engine`
+ * (scheduler.py:198-205,350,372; model.py:115-183) plus the page pool and
+ * prune entry points it drives (paging.py:27-107, pruning.py:102-133).  Every
+ * function below replaces one piece of that interface; the citation on each
+ * names the reference code it replaces.  All pointers are device pointers
+ * unless noted, sizes are plain integers, `stream` is a cudaStream_t passed as
+ * void*.  No function synchronises the host except tim_read_error().
+ *
+ * Step descriptor.  One engine step is described by a single int32 buffer
+ * (`step`, device-resident, uploaded with one H2D copy) that starts with a
+ * tim_step_header; record arrays follow at the header's offsets.  All kernels
+ * of a step read the same buffer, so the host never re-uploads metadata and
+ * the whole step is CUDA-graph capturable.
+ */
+#ifndef TIMRUN_H
+#define TIMRUN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes.  Each maps onto the reference exception named beside it. */
+enum {
+  TIM_OK = 0,
+  TIM_OUT_OF_PAGES = 1,       /* paging.py:14-18   OutOfPages(needed, available) */
+  TIM_DOUBLE_FREE = 2,        /* paging.py:21-24   DoubleFree(page_id)           */
+  TIM_POSITION_OVERFLOW = 3,  /* model.py:24-28    PositionOverflow(pos, limit)  */
+  TIM_SPAN_OUT_OF_RANGE = 4,  /* pruning.py:25-26  SpanOutOfRange (desync)       */
+  TIM_BAD_ARGUMENT = 5,       /* ValueError                                      */
+  TIM_CUDA_ERROR = 6,
+  TIM_UNSUPPORTED = 7
+};
+
+enum { TIM_DTYPE_F32 = 0, TIM_DTYPE_BF16 = 1 };
+
+/* Page-op kinds (records in the step descriptor). */
+enum {
+  TIM_OP_ALLOC = 0,  /* pop `count` ids off the LIFO free stack (paging.py:52-60) into table[slot][off..] */
+  TIM_OP_FREE = 1    /* push table[slot][off..off+count) in table order (paging.py:62-67)          */
+};
+
+/* Header of the per-step descriptor.  Offsets are int32 element offsets into
+ * the same buffer.  Record layouts (int32 fields):
+ *   new   : {slot, logical_idx, token, row, live_idx}          host-known tokens
+ *   seg   : {slot, m, n, row_off}                               one encode segment
+ *   dec   : {row, slot, kv_len}  + dec_prefix[n_dec+1]          split-K decode queries
+ *   ext   : {row_off, slot, m, n, q0}                           extend q-tiles
+ *   job   : {slot, old_len, suffix_start, reencode_from,
+ *            span_off, n_spans, out_row, expect_keep}           prune compaction jobs
+ *   spans : {start, end}                                        coalesced evict spans
+ *   op    : {kind, slot, table_off, count, sp_before}           page ops
+ *   phase : n_phases+1 op offsets (ops within a phase are independent)
+ *   last  : {row}                                               rows whose logits are produced
+ */
+typedef struct {
+  int32_t n_rows, n_rows_pad;
+  int32_t n_new, n_segs, n_dec, n_ext, n_jobs, n_ops, n_phases, n_last;
+  int32_t dec_total;
+  int32_t off_new, off_segs, off_dec, off_dec_prefix, off_ext, off_jobs, off_spans;
+  int32_t off_ops, off_phases, off_last;
+  int32_t reserved[11];
+} tim_step_header;  /* 32 int32 */
+
+#define TIM_NEW_FIELDS 5
+#define TIM_SEG_FIELDS 4
+#define TIM_DEC_FIELDS 3
+#define TIM_EXT_FIELDS 5
+#define TIM_JOB_FIELDS 8
+#define TIM_OP_FIELDS 5
+
+/* ---------------------------------------------------------------- utility */
+int32_t tim_abi_version(void);
+const char* tim_last_error(void);               /* host string of the last failure */
+int32_t tim_sm_count(void);                     /* SMs of the current device */
+/* Blocking read of the device error word (err[0] code, err[1] detail); clears it. */
+int32_t tim_read_error(int32_t* err_dev, int32_t* code_out, int32_t* detail_out, void* stream);
+
+/* ------------------------------------------------------ pool / allocator (K5) */
+/* Free stack initialised to [cap-1, ..., 0] so pops return 0,1,2,... (paging.py:40),
+ * owner[] = -1 (paging.py:41). */
+int32_t tim_pool_init(int32_t* free_stack, int32_t* owner, int32_t capacity, void* stream);
+
+/* K5 + K4-free: run the step's phased page ops against the device LIFO free stack.
+ * ALLOC pops ids top-first (paging.py:57), FREE pushes table entries in table
+ * order (paging.py:62-67, pruning.py:130 truncate_from, scheduler.py:398,522,539).
+ * Owner checks raise TIM_DOUBLE_FREE in err[]; stack under/overflow raises
+ * TIM_OUT_OF_PAGES.  One CTA; phases are separated by block barriers. */
+int32_t tim_page_ops(const int32_t* step, int32_t* free_stack, int32_t* owner, int32_t capacity,
+                     int32_t* block_tables, int64_t table_stride, int32_t* err, void* stream);
+
+/* -------------------------------------------------------- subtask prune (K4) */
+/* For each prune job: verify suffix_start against live[] (the first index with
+ * live >= reencode_from, pruning.py:126-128), mark retained entries of
+ * live[s:old_len) not covered by the coalesced evict spans (pruning.py:131),
+ * compact them in place (new_live[s:]), and gather their token ids from the
+ * device logical stream into the step's row_tokens at out_row
+ * (pruning.py:132 suffix_tokens; scheduler.py:403-405).  Count mismatches
+ * against the host plan raise TIM_SPAN_OUT_OF_RANGE. */
+int32_t tim_prune_compact(const int32_t* step, int32_t max_jobs, int32_t* live, int64_t live_stride,
+                          const int32_t* logical, int64_t logical_stride, int32_t* row_tokens,
+                          int32_t* err, void* stream);
+
+/* Stage the step's rows: write host-known new tokens into the device logical
+ * stream, live[] and row_tokens; then for every segment row compute its page
+ * (table[slot][m+i], appended by the ALLOC ops) and position m+i (position
+ * recycling: scheduler.py:366-372, model.py:174-179).  Rows past n_rows up to
+ * n_rows_pad get page -1 (no KV write). */
+int32_t tim_stage_rows(const int32_t* step, const int32_t* block_tables, int64_t table_stride,
+                       int32_t* live, int64_t live_stride, int32_t* logical, int64_t logical_stride,
+                       int32_t* row_tokens, int32_t* row_pages, int32_t* row_pos, void* stream);
+
+/* ------------------------------------------------------- model-side kernels */
+/* h[r,:] = emb[row_tokens[r], :]  (model.py:138) */
+int32_t tim_embed(const int32_t* row_tokens, int32_t n_rows, const void* emb, int32_t dm,
+                  void* h, int32_t dtype, void* stream);
+/* y = x / sqrt(mean(x^2) + eps) (model.py:69-70); fp32 math, rows of length dm. */
+int32_t tim_rmsnorm(const void* x, int64_t x_stride, void* y, int64_t y_stride, int32_t n_rows,
+                    int32_t dm, float eps, int32_t dtype, void* stream);
+/* in-place x = x / (1 + exp(-x)) (model.py:73-74) */
+int32_t tim_silu(void* x, int64_t n, int32_t dtype, void* stream);
+
+/* K3: rotate-half RoPE (model.py:118-125) of q and k from the fused qkv GEMM
+ * output [rows, (hq + 2 hkv) * D], store roped K and raw V into the page of
+ * each row for this layer (model.py:147-148), write roped q to q_out.
+ * cos/sin tables are [position_limit, D/2] fp32, built on the host exactly as
+ * the reference (fp32 angle pos*inv_freq, model.py:104-105,121). */
+int32_t tim_rope_kv_store(const void* qkv, int32_t n_rows, const int32_t* row_pos,
+                          const int32_t* row_pages, const float* cos_tab, const float* sin_tab,
+                          int32_t hq, int32_t hkv, int32_t head_dim, void* q_out,
+                          void* k_layer, void* v_layer, int32_t dtype, void* stream);
+
+/* K1+K6: split-K (stream-K) paged GQA decode attention over retained pages only
+ * (model.py:149-159 with n = 1).  `n_ctas` persistent CTAs split the
+ * concatenated kv tokens of all decode queries evenly; queries spanning several
+ * CTAs are merged in-kernel by the last CTA (log-sum-exp combine).
+ * ws: float workspace of tim_decode_ws_floats(n_ctas, n_dec, hq, D) floats;
+ * counters: int32[max_dec] zero-initialised once (self-resetting); max_dec bounds n_dec. */
+int64_t tim_decode_ws_floats(int32_t n_ctas, int32_t max_dec, int32_t hq, int32_t head_dim);
+int32_t tim_attn_decode(const int32_t* step, const void* q, void* out, const void* k_layer,
+                        const void* v_layer, const int32_t* block_tables, int64_t table_stride,
+                        int32_t hq, int32_t hkv, int32_t head_dim, float scale, float* ws,
+                        int32_t* counters, int32_t n_ctas, int32_t max_dec, int32_t dtype,
+                        void* stream);
+
+/* K2: extend / re-encode attention: q-tiles of a multi-token segment attend the
+ * paged prefix table[slot][0..m) plus the causal new block (model.py:139-140,155). */
+int32_t tim_attn_extend(const int32_t* step, int32_t max_items, const void* q, void* out,
+                        const void* k_layer, const void* v_layer, const int32_t* block_tables,
+                        int64_t table_stride, int32_t hq, int32_t hkv, int32_t head_dim,
+                        float scale, int32_t dtype, void* stream);
+/* Queries per extend item for a given config (the host tiles segments with it). */
+int32_t tim_extend_queries_per_item(int32_t hq, int32_t hkv, int32_t head_dim, int32_t dtype);
+
+/* Greedy argmax over rows of logits [n, vocab] (lowest id on ties, model.py:186-192). */
+int32_t tim_argmax(const void* logits, int32_t n_rows, int32_t vocab, int32_t* out,
+                   int32_t dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TIMRUN_H */

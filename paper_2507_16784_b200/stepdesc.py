@@ -1,0 +1,98 @@
+"""Host-side builder of the per-step descriptor (tim_step_header + records).
+
+The host plans a step purely in counts; the descriptor is the single int32
+buffer every kernel of the step reads (include/timrun.h).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib as L
+
+_HDR = [
+    "n_rows", "n_rows_pad", "n_new", "n_segs", "n_dec", "n_ext", "n_jobs", "n_ops", "n_phases",
+    "n_last", "dec_total", "off_new", "off_segs", "off_dec", "off_dec_prefix", "off_ext", "off_jobs",
+    "off_spans", "off_ops", "off_phases", "off_last",
+]
+
+
+class StepDesc:
+    """Accumulates one step's records and packs them into an int32 array."""
+
+    __slots__ = ("new", "segs", "dec", "ext", "jobs", "spans", "ops", "phase_starts", "last",
+                 "n_rows", "_last_kind")
+
+    def __init__(self):
+        self.new: list = []      # (slot, logical_idx, token, row, live_idx)
+        self.segs: list = []     # (slot, m, n, row_off)
+        self.dec: list = []      # (row, slot, kv_len)
+        self.ext: list = []      # (row_off, slot, m, n, q0)
+        self.jobs: list = []     # (slot, old_len, s, reencode_from, span_off, n_spans, out_row, keep)
+        self.spans: list = []    # start, end (flattened pairs)
+        self.ops: list = []      # (kind, slot, table_off, count, sp_before)
+        self.phase_starts: list = []
+        self.last: list = []     # rows whose logits are produced
+        self.n_rows = 0
+        self._last_kind = -1
+
+    # ------------------------------------------------------------- page ops
+    def op(self, kind: int, slot: int, table_off: int, count: int, sp_before: int) -> None:
+        if count <= 0:
+            return
+        if kind != self._last_kind:
+            self.phase_starts.append(len(self.ops))
+            self._last_kind = kind
+        self.ops.append((kind, slot, table_off, count, sp_before))
+
+    def job(self, slot, old_len, s, reencode_from, spans, out_row, keep) -> None:
+        off = len(self.spans) // 2
+        for a, b in spans:
+            self.spans.extend((a, b))
+        self.jobs.append((slot, old_len, s, reencode_from, off, len(spans), out_row, keep))
+
+    # ---------------------------------------------------------------- pack
+    def pack(self, n_rows_pad: int | None = None) -> np.ndarray:
+        parts = []
+        off = L.HEADER_INTS
+        hdr = dict.fromkeys(_HDR, 0)
+
+        def add(name, rows, width):
+            nonlocal off
+            arr = np.asarray(rows, dtype=np.int32).reshape(-1)
+            if width:
+                assert arr.size == len(rows) * width
+            hdr["off_" + name] = off
+            parts.append(arr)
+            off += arr.size
+
+        add("new", self.new, L.NEW_FIELDS)
+        add("segs", self.segs, L.SEG_FIELDS)
+        add("dec", self.dec, L.DEC_FIELDS)
+        prefix = np.zeros(len(self.dec) + 1, dtype=np.int64)
+        if self.dec:
+            prefix[1:] = np.cumsum([d[2] for d in self.dec])
+        assert prefix[-1] < 2**31
+        hdr["off_dec_prefix"] = off
+        parts.append(prefix.astype(np.int32))
+        off += prefix.size
+        add("ext", self.ext, L.EXT_FIELDS)
+        add("jobs", self.jobs, L.JOB_FIELDS)
+        add("spans", self.spans, 0)
+        add("ops", self.ops, L.OP_FIELDS)
+        phases = list(self.phase_starts) + [len(self.ops)]
+        hdr["off_phases"] = off
+        parts.append(np.asarray(phases, dtype=np.int32))
+        off += len(phases)
+        add("last", self.last, 0)
+        hdr.update(
+            n_rows=self.n_rows,
+            n_rows_pad=self.n_rows if n_rows_pad is None else n_rows_pad,
+            n_new=len(self.new), n_segs=len(self.segs), n_dec=len(self.dec), n_ext=len(self.ext),
+            n_jobs=len(self.jobs), n_ops=len(self.ops), n_phases=len(self.phase_starts),
+            n_last=len(self.last), dec_total=int(prefix[-1]),
+        )
+        head = np.zeros(L.HEADER_INTS, dtype=np.int32)
+        for i, k in enumerate(_HDR):
+            head[i] = hdr[k]
+        return np.concatenate([head] + parts)

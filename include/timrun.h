@@ -55,7 +55,7 @@ enum {
  *   job   : {slot, old_len, suffix_start, reencode_from,
  *            span_off, n_spans, out_row, expect_keep}           prune compaction jobs
  *   spans : {start, end}                                        coalesced evict spans
- *   op    : {kind, slot, table_off, count, sp_before}           page ops
+ *   op    : {kind, slot, table_off, count, sp_before, owner}    page ops (owner -2: any)
  *   phase : n_phases+1 op offsets (ops within a phase are independent)
  *   last  : {row}                                               rows whose logits are produced
  */
@@ -73,7 +73,7 @@ typedef struct {
 #define TIM_DEC_FIELDS 3
 #define TIM_EXT_FIELDS 5
 #define TIM_JOB_FIELDS 8
-#define TIM_OP_FIELDS 5
+#define TIM_OP_FIELDS 6
 
 /* ---------------------------------------------------------------- utility */
 int32_t tim_abi_version(void);

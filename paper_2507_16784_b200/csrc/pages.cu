@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(1024) page_ops_kernel(const int32_t* step, int
     for (int o = o0 + warp; o < o1; o += nwarps) {
       const int32_t* op = ops + (int64_t)o * TIM_OP_FIELDS;
       const int32_t kind = op[0], slot = op[1], toff = op[2], count = op[3], sp = op[4];
+      const int32_t who = op[5];
       int32_t* trow = tables + (int64_t)slot * tstride + toff;
       if (kind == TIM_OP_ALLOC) {
         if (sp - count < 0) {
@@ -44,7 +45,7 @@ __global__ void __launch_bounds__(1024) page_ops_kernel(const int32_t* step, int
         }
         for (int j = lane; j < count; j += 32) {
           const int32_t page = free_stack[sp - 1 - j];
-          if (page < 0 || page >= capacity || atomicExch(&owner[page], slot) != -1)
+          if (page < 0 || page >= capacity || atomicExch(&owner[page], who) != -1)
             raise_error(err, TIM_DOUBLE_FREE, page);
           trow[j] = page;
         }
@@ -55,8 +56,12 @@ __global__ void __launch_bounds__(1024) page_ops_kernel(const int32_t* step, int
         }
         for (int j = lane; j < count; j += 32) {
           const int32_t page = trow[j];
-          if (page < 0 || page >= capacity || atomicCAS(&owner[page], slot, -1) != slot)
-            raise_error(err, TIM_DOUBLE_FREE, page);
+          bool ok = page >= 0 && page < capacity;
+          if (ok) {
+            if (who == -2) ok = atomicExch(&owner[page], -1) != -1;
+            else ok = atomicCAS(&owner[page], who, -1) == who;
+          }
+          if (!ok) raise_error(err, TIM_DOUBLE_FREE, page);
           free_stack[sp + j] = page;
         }
       }
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(256) prune_compact_kernel(const int32_t* step,
     __syncthreads();  // every read of this chunk happened before any in-place write
     if (keep) {
       lrow[s + kept + rank] = val;
-      row_tokens[out_row + kept + rank] = grow[val];
+      if (out_row >= 0) row_tokens[out_row + kept + rank] = grow[val];
     }
     kept += total;
     __syncthreads();

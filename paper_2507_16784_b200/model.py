@@ -1,0 +1,530 @@
+"""Model backends on the B200 (drop-in for threadrun/model.py) and the step runtime.
+
+`B200Transformer` implements the reference backend protocol (position_limit,
+make_pool, prefill, extend, decode_step; model.py:115-183) with the same
+arithmetic as TinyTransformer (weightless RMSNorm, rotate-half RoPE, causal
+attention over page-size-1 pages, non-gated SiLU MLP, tied logits), extended
+with GQA (`kv_heads`) and an MLP width field (`mlp_dim`) for the Qwen3-8B
+shaped configuration.  With weight_init="reference" the weights are drawn from
+the reference's numpy RNG stream (model.py:87-103), so fp32 runs reproduce the
+reference to rounding.
+
+`StepRuntime` owns the device state of a batched engine: block tables, live
+lists and logical token streams per request slot, row buffers, activations
+and the decode workspace.  One engine step = one descriptor upload + K4
+(prune compaction) + K5 (page ops) + row staging + one batched forward over
+every request's new tokens (mixed decode / re-encode / prefill rows).
+GEMMs go to cuBLAS through torch; attention, RoPE+KV store, paging and the
+per-row kernels are libtimrun.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import asdict, dataclass
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .paging import DevicePagePool, PageTable, raise_device_error, stream_handle
+from .stepdesc import StepDesc
+
+
+class PositionOverflow(RuntimeError):
+    def __init__(self, position: int, limit: int):
+        super().__init__(f"position {position} >= limit {limit}")
+        self.position = position
+        self.limit = limit
+
+
+class EmptyExtend(ValueError):
+    pass
+
+
+class EmptyMask(RuntimeError):
+    """Grammar dead end: no token admissible."""
+
+
+@dataclass
+class ModelConfig:
+    layers: int = 2
+    heads: int = 4
+    head_dim: int = 16
+    vocab: int = 512
+    position_limit: int = 256
+    rope_base: float = 10000.0
+    seed: int = 0
+    precision: str = "float32"       # "float32" | "bfloat16"
+    kv_heads: int = 0                # 0: same as heads (reference)
+    mlp_dim: int = 0                 # 0: 4 * model_dim (reference)
+    weight_init: str = "reference"   # "reference" (numpy stream) | "device" (torch RNG on GPU)
+
+    @property
+    def model_dim(self) -> int:
+        return self.heads * self.head_dim
+
+    @property
+    def n_kv(self) -> int:
+        return self.kv_heads or self.heads
+
+    @property
+    def n_mlp(self) -> int:
+        return self.mlp_dim or 4 * self.model_dim
+
+    @property
+    def dtype(self):
+        return np.float64 if self.precision == "float64" else np.float32
+
+    @property
+    def torch_dtype(self):
+        return {"float32": torch.float32, "bfloat16": torch.bfloat16}[self.precision]
+
+    @property
+    def tim_dtype(self) -> int:
+        return L.DTYPE_BF16 if self.precision == "bfloat16" else L.DTYPE_F32
+
+    def kv_shape(self) -> tuple[int, int, int]:
+        return (self.layers, self.n_kv, self.head_dim)
+
+    def kv_bytes_per_token(self) -> int:
+        """K + V bytes of one working-memory token over all layers."""
+        return 2 * self.layers * self.n_kv * self.head_dim * (2 if self.precision == "bfloat16" else 4)
+
+    def to_json_file(self, path) -> None:
+        Path(path).write_text(json.dumps(asdict(self), indent=2))
+
+    @classmethod
+    def from_json_file(cls, path) -> "ModelConfig":
+        return cls(**json.loads(Path(path).read_text()))
+
+
+def qwen3_8b_shape(**over) -> ModelConfig:
+    """Qwen3-8B-shaped TIM decoder (BASELINE config 2): 36 layers, hidden 4096,
+    32 q / 8 kv heads of 128, MLP 12288, rope base 1e6, bf16, vocab 512."""
+    kw = dict(layers=36, heads=32, kv_heads=8, head_dim=128, mlp_dim=12288, vocab=512,
+              position_limit=40960, rope_base=1e6, precision="bfloat16", weight_init="device")
+    kw.update(over)
+    return ModelConfig(**kw)
+
+
+def _reference_weights(cfg: ModelConfig):
+    """numpy draw in the order of model.py:91-103 (emb, then wq wk wv wo w1 w2 per layer)."""
+    dm = cfg.model_dim
+    rng = np.random.default_rng(cfg.seed)
+    scale = 1.0 / np.sqrt(dm)
+
+    def mat(*shape):
+        return (rng.standard_normal(shape) * scale).astype(np.float32)
+
+    emb = mat(cfg.vocab, dm)
+    kvd = cfg.n_kv * cfg.head_dim
+    layers = []
+    for _ in range(cfg.layers):
+        layers.append([mat(dm, dm), mat(dm, kvd), mat(dm, kvd), mat(dm, dm),
+                       mat(dm, cfg.n_mlp), mat(cfg.n_mlp, dm)])
+    return emb, layers
+
+
+def _rope_tables(cfg: ModelConfig):
+    """cos/sin of the fp32 angle pos*inv_freq, inv_freq built as model.py:104-105."""
+    half = cfg.head_dim // 2
+    inv = (cfg.rope_base ** (-np.arange(half) / half)).astype(np.float32)
+    pos = np.arange(cfg.position_limit, dtype=np.float32)
+    ang = pos[:, None] * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+class StepRuntime:
+    """Device state + executor of batched engine steps for one pool."""
+
+    def __init__(self, model, pool: DevicePagePool, max_slots: int, logical_cap: int):
+        self.model = model
+        self.pool = pool
+        self.dev = pool.device
+        P = model.position_limit
+        self.max_slots = max_slots
+        self.scratch_slot = max_slots
+        S = max_slots + 1
+        self.tables = torch.full((S, P), -1, dtype=torch.int32, device=self.dev)
+        self.live = torch.zeros((S, P), dtype=torch.int32, device=self.dev)
+        self.logical = torch.zeros((S, max(logical_cap, 1)), dtype=torch.int32, device=self.dev)
+        self.counters = torch.zeros(S + 1, dtype=torch.int32, device=self.dev)
+        self._rows = 0
+        self._step_cap = 0
+        self.step_dev = None
+        self.step_host = None
+        self.sms = L.load().tim_sm_count()
+        self.last_tokens = None
+        self.last_logits = None
+        self.launches = 0
+        self._last_upload_bytes = 0
+        self.recording = None        # list -> record descriptors instead of executing
+        self.attn_events = None      # list -> CUDA events around layer-0 decode attention
+
+    # ----------------------------------------------------------- buffers
+    def _ensure_rows(self, n: int) -> None:
+        if n <= self._rows:
+            return
+        R = 1 << max(6, (n - 1).bit_length())
+        d = self.dev
+        self.row_tokens = torch.zeros(R, dtype=torch.int32, device=d)
+        self.row_pages = torch.full((R,), -1, dtype=torch.int32, device=d)
+        self.row_pos = torch.zeros(R, dtype=torch.int32, device=d)
+        if self.model is not None and self.model.has_weights:
+            self.model.alloc_activations(self, R)
+        self._rows = R
+
+    def upload(self, arr: np.ndarray) -> torch.Tensor:
+        """Copy a packed descriptor to the device through a ring of pinned
+        buffers; a buffer is rewritten only after its previous copy completed."""
+        n = arr.size
+        if n > self._step_cap:
+            cap = 1 << max(10, (n - 1).bit_length())
+            self._ring = [torch.empty(cap, dtype=torch.int32, pin_memory=True) for _ in range(4)]
+            self._ring_ev = [None] * 4
+            self._ring_i = 0
+            self.step_dev = torch.empty(cap, dtype=torch.int32, device=self.dev)
+            self._step_cap = cap
+        i = self._ring_i
+        self._ring_i = (i + 1) % len(self._ring)
+        ev = self._ring_ev[i]
+        if ev is not None:
+            ev.synchronize()
+        host = self._ring[i]
+        host[:n].numpy()[:] = arr
+        self._last_upload_bytes = n * 4
+        self.step_dev[:n].copy_(host[:n], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._ring_ev[i] = ev
+        return self.step_dev
+
+    # -------------------------------------------------------------- step
+    def run_step(self, sd: StepDesc, forward: bool = True):
+        """Execute one planned step; returns the greedy tokens of sd.last rows
+        (device tensor) or None when there is nothing to encode.  In record
+        mode the packed descriptor is only stored (see replay)."""
+        arr = sd.pack()
+        self._ensure_rows(max(sd.n_rows, 1))
+        if self.recording is not None:
+            self.recording.append((sd, arr, forward))
+            return None
+        return self._execute(sd, self.upload(arr), forward)
+
+    def _execute(self, sd: StepDesc, step: torch.Tensor, forward: bool):
+        st = stream_handle()
+        tstride = self.tables.shape[1]
+        if sd.jobs:
+            L.call("tim_prune_compact", step.data_ptr(), len(sd.jobs), self.live.data_ptr(),
+                   self.live.shape[1], self.logical.data_ptr(), self.logical.shape[1],
+                   self.row_tokens.data_ptr(), self.pool.err.data_ptr(), st)
+            self.launches += 1
+        if sd.ops:
+            self.pool.run_ops(step, self.tables)
+            self.launches += 1
+        if sd.new or sd.n_rows:
+            L.call("tim_stage_rows", step.data_ptr(), self.tables.data_ptr(), tstride,
+                   self.live.data_ptr(), self.live.shape[1], self.logical.data_ptr(),
+                   self.logical.shape[1], self.row_tokens.data_ptr(), self.row_pages.data_ptr(),
+                   self.row_pos.data_ptr(), st)
+            self.launches += 2
+        if not forward or sd.n_rows == 0 or self.model is None or not self.model.has_weights:
+            return None
+        return self.model.forward_rows(self, step, sd)
+
+    def replay_upload(self, records) -> list:
+        """Make recorded descriptors device-resident (one buffer, one copy)."""
+        offs, total = [], 0
+        for _, arr, _ in records:
+            offs.append(total)
+            total += (arr.size + 31) // 32 * 32
+        host = np.zeros(max(total, 1), dtype=np.int32)
+        for (_, arr, _), o in zip(records, offs):
+            host[o:o + arr.size] = arr
+        dev = torch.from_numpy(host).to(self.dev)
+        return [(sd, dev[o:o + arr.size], fw) for (sd, arr, fw), o in zip(records, offs)]
+
+    def replay(self, resident) -> None:
+        for sd, step, fw in resident:
+            self._execute(sd, step, fw)
+
+    def check(self) -> None:
+        self.pool.check()
+
+
+class B200Transformer:
+    """TinyTransformer-compatible backend running on libtimrun + cuBLAS."""
+
+    has_weights = True
+
+    def __init__(self, config: ModelConfig, device: str = "cuda"):
+        if config.precision not in ("float32", "bfloat16"):
+            raise NotImplementedError(f"precision {config.precision!r} is not supported on the B200 path")
+        L.load()
+        self.config = cfg = config
+        self.dev = torch.device(device)
+        dt = cfg.torch_dtype
+        dm, D, hq, hkv = cfg.model_dim, cfg.head_dim, cfg.heads, cfg.n_kv
+        if cfg.precision == "float32":
+            torch.backends.cuda.matmul.allow_tf32 = False
+            torch.backends.cudnn.allow_tf32 = False
+        if cfg.weight_init == "reference":
+            emb, layers = _reference_weights(cfg)
+            self.emb = torch.from_numpy(emb).to(self.dev, dt)
+            self.wqkv, self.wo, self.w1, self.w2 = [], [], [], []
+            for wq, wk, wv, wo, w1, w2 in layers:
+                self.wqkv.append(torch.from_numpy(np.concatenate([wq, wk, wv], axis=1)).to(self.dev, dt))
+                self.wo.append(torch.from_numpy(wo).to(self.dev, dt))
+                self.w1.append(torch.from_numpy(w1).to(self.dev, dt))
+                self.w2.append(torch.from_numpy(w2).to(self.dev, dt))
+        else:
+            g = torch.Generator(device=self.dev).manual_seed(cfg.seed)
+            sc = 1.0 / math.sqrt(dm)
+
+            def mat(*shape):
+                return (torch.randn(*shape, generator=g, device=self.dev, dtype=torch.float32) * sc).to(dt)
+
+            self.emb = mat(cfg.vocab, dm)
+            W = (hq + 2 * hkv) * D
+            self.wqkv = [mat(dm, W) for _ in range(cfg.layers)]
+            self.wo = [mat(dm, dm) for _ in range(cfg.layers)]
+            self.w1 = [mat(dm, cfg.n_mlp) for _ in range(cfg.layers)]
+            self.w2 = [mat(cfg.n_mlp, dm) for _ in range(cfg.layers)]
+        self.emb_t32 = self.emb.float().t().contiguous()
+        cos, sin = _rope_tables(cfg)
+        self.cos = torch.from_numpy(cos).to(self.dev)
+        self.sin = torch.from_numpy(sin).to(self.dev)
+        self.scale = 1.0 / math.sqrt(D)
+        self.tensor_cores = (cfg.precision == "bfloat16" and L.load().tim_extend_queries_per_item(
+            hq, hkv, D, L.DTYPE_BF16) < (1 << 30))
+        self.qpi = L.load().tim_extend_queries_per_item(hq, hkv, D, cfg.tim_dtype)
+        self._runtimes: dict[int, StepRuntime] = {}
+
+    # ------------------------------------------------------- protocol
+    @property
+    def vocab_size(self) -> int:
+        return self.config.vocab
+
+    @property
+    def position_limit(self) -> int:
+        return self.config.position_limit
+
+    def make_pool(self, capacity: int) -> DevicePagePool:
+        return DevicePagePool(capacity, kv_shape=self.config.kv_shape(),
+                              dtype=self.config.torch_dtype, device=self.dev)
+
+    def runtime(self, pool: DevicePagePool, max_slots: int, logical_cap: int) -> StepRuntime:
+        return StepRuntime(self, pool, max_slots, logical_cap)
+
+    def weight_bytes(self) -> int:
+        t = [self.emb] + self.wqkv + self.wo + self.w1 + self.w2
+        return sum(x.numel() * x.element_size() for x in t)
+
+    def _protocol_runtime(self, pool: DevicePagePool) -> StepRuntime:
+        rt = self._runtimes.get(id(pool))
+        if rt is None or rt.pool is not pool:
+            rt = StepRuntime(self, pool, 0, 1)
+            self._runtimes[id(pool)] = rt
+        return rt
+
+    def _forward(self, tokens, positions, table: PageTable, pool: DevicePagePool):
+        cfg = self.config
+        n = len(tokens)
+        for p in positions:
+            if p >= cfg.position_limit:
+                raise PositionOverflow(int(p), cfg.position_limit)
+        new_pages = pool.alloc(table.request_id, n)
+        rt = self._protocol_runtime(pool)
+        m = len(table.pages)
+        pages = list(table.pages) + new_pages
+        rt._ensure_rows(n)
+        rt.tables[rt.scratch_slot, : m + n] = torch.tensor(pages, dtype=torch.int32, device=self.dev)
+        rt.row_tokens[:n] = torch.tensor(tokens, dtype=torch.int32, device=self.dev)
+        rt.row_pages[:n] = torch.tensor(new_pages, dtype=torch.int32, device=self.dev)
+        rt.row_pos[:n] = torch.tensor([int(p) for p in positions], dtype=torch.int32, device=self.dev)
+        sd = StepDesc()
+        sd.n_rows = n
+        self.plan_attention(sd, rt.scratch_slot, m, n, 0)
+        sd.last.append(n - 1)
+        step = rt.upload(sd.pack())
+        self.forward_rows(rt, step, sd)
+        table.append(new_pages)
+        return rt.last_logits[0].cpu().numpy()
+
+    def prefill(self, tokens, positions, table, pool):
+        if len(tokens) != len(positions):
+            raise ValueError("tokens and positions must align")
+        if not tokens:
+            raise EmptyExtend("nothing to prefill")
+        return self._forward(list(tokens), list(positions), table, pool)
+
+    def extend(self, tokens, start_position, table, pool):
+        if not tokens:
+            raise EmptyExtend("nothing to extend")
+        return self._forward(list(tokens), list(range(start_position, start_position + len(tokens))),
+                             table, pool)
+
+    def decode_step(self, last_token, position, table, pool):
+        return self._forward([last_token], [position], table, pool)
+
+    # ------------------------------------------------------ batched path
+    def plan_attention(self, sd: StepDesc, slot: int, m: int, n: int, row_off: int) -> None:
+        """Attention work records for one segment: split-K decode for single-row
+        tensor-core segments, q-tiles for the rest."""
+        sd.segs.append((slot, m, n, row_off))
+        if self.tensor_cores and n == 1:
+            sd.dec.append((row_off, slot, m + 1))
+        elif self.tensor_cores:
+            for q0 in range(0, n, self.qpi):
+                sd.ext.append((row_off, slot, m, n, q0))
+
+    def alloc_activations(self, rt: StepRuntime, R: int) -> None:
+        cfg = self.config
+        dt, d = cfg.torch_dtype, self.dev
+        dm, D = cfg.model_dim, cfg.head_dim
+        W = (cfg.heads + 2 * cfg.n_kv) * D
+        rt.h = torch.zeros(R, dm, dtype=dt, device=d)
+        rt.x = torch.zeros(R, dm, dtype=dt, device=d)
+        rt.qkv = torch.zeros(R, W, dtype=dt, device=d)
+        rt.q = torch.zeros(R, cfg.heads * D, dtype=dt, device=d)
+        rt.ctx = torch.zeros(R, cfg.heads * D, dtype=dt, device=d)
+        rt.u = torch.zeros(R, cfg.n_mlp, dtype=dt, device=d)
+        n_ctas = max(rt.sms, 1)
+        rt.n_ctas = n_ctas
+        rt.max_dec = R
+        rt.ws = torch.zeros(L.load().tim_decode_ws_floats(n_ctas, R, cfg.heads, D), device=d)
+        rt.counters = torch.zeros(R, dtype=torch.int32, device=d)
+
+    def forward_rows(self, rt: StepRuntime, step: torch.Tensor, sd: StepDesc):
+        """The batched forward over staged rows (model.py:137-164 for every segment)."""
+        cfg = self.config
+        T = sd.n_rows
+        st = stream_handle()
+        td = cfg.tim_dtype
+        dm, D, hq, hkv = cfg.model_dim, cfg.head_dim, cfg.heads, cfg.n_kv
+        h, x, qkv, q, ctx, u = rt.h[:T], rt.x[:T], rt.qkv[:T], rt.q, rt.ctx[:T], rt.u[:T]
+        sp = step.data_ptr()
+        L.call("tim_embed", rt.row_tokens.data_ptr(), T, self.emb.data_ptr(), dm, h.data_ptr(), td, st)
+        tstride = rt.tables.shape[1]
+        launches = 1
+        for li in range(cfg.layers):
+            kl = self.pool_layer(rt.pool.K_layers, li)
+            vl = self.pool_layer(rt.pool.V_layers, li)
+            L.call("tim_rmsnorm", h.data_ptr(), dm, x.data_ptr(), dm, T, dm, 1e-6, td, st)
+            torch.matmul(x, self.wqkv[li], out=qkv)
+            L.call("tim_rope_kv_store", qkv.data_ptr(), T, rt.row_pos.data_ptr(),
+                   rt.row_pages.data_ptr(), self.cos.data_ptr(), self.sin.data_ptr(), hq, hkv, D,
+                   q.data_ptr(), kl, vl, td, st)
+            launches += 2
+            if self.tensor_cores:
+                if sd.dec:
+                    timed = li == 0 and rt.attn_events is not None
+                    if timed:
+                        e0 = torch.cuda.Event(enable_timing=True)
+                        e0.record()
+                    L.call("tim_attn_decode", sp, q.data_ptr(), ctx.data_ptr(), kl, vl,
+                           rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, rt.ws.data_ptr(),
+                           rt.counters.data_ptr(), rt.n_ctas, rt.max_dec, td, st)
+                    launches += 1
+                    if timed:
+                        e1 = torch.cuda.Event(enable_timing=True)
+                        e1.record()
+                        rt.attn_events.append((e0, e1, sd))
+                if sd.ext:
+                    L.call("tim_attn_extend", sp, len(sd.ext), q.data_ptr(), ctx.data_ptr(), kl, vl,
+                           rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, td, st)
+                    launches += 1
+            else:
+                L.call("tim_attn_extend", sp, T, q.data_ptr(), ctx.data_ptr(), kl, vl,
+                       rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, td, st)
+                launches += 1
+            h.addmm_(ctx, self.wo[li])
+            L.call("tim_rmsnorm", h.data_ptr(), dm, x.data_ptr(), dm, T, dm, 1e-6, td, st)
+            torch.matmul(x, self.w1[li], out=u)
+            L.call("tim_silu", u.data_ptr(), u.numel(), td, st)
+            h.addmm_(u, self.w2[li])
+            launches += 2
+        n_last = len(sd.last)
+        off = sd.offsets["off_last"]
+        idx = step[off: off + n_last].long()
+        hl = h.index_select(0, idx)
+        xl = torch.empty_like(hl)
+        L.call("tim_rmsnorm", hl.data_ptr(), dm, xl.data_ptr(), dm, n_last, dm, 1e-6, td, st)
+        logits = torch.matmul(xl.float(), self.emb_t32)
+        toks = torch.empty(n_last, dtype=torch.int32, device=self.dev)
+        L.call("tim_argmax", logits.data_ptr(), n_last, cfg.vocab, toks.data_ptr(), L.DTYPE_F32, st)
+        launches += 2
+        rt.launches += launches
+        rt.last_logits = logits
+        rt.last_tokens = toks
+        return toks
+
+    @staticmethod
+    def pool_layer(t: torch.Tensor, li: int) -> int:
+        return t.data_ptr() + li * t.stride(0) * t.element_size()
+
+
+# Reference-compatible name for the numeric backend.
+TinyTransformer = B200Transformer
+
+
+class ScriptedModel:
+    """Replay backend: device page accounting (K4/K5) without arithmetic
+    (model.py:195-233).  Logits are None; the engine pops the script."""
+
+    has_weights = False
+
+    def __init__(self, vocab: int = 512, position_limit: int = 256):
+        self.vocab = vocab
+        self.position_limit = position_limit
+        self.config = None
+
+    @property
+    def vocab_size(self) -> int:
+        return self.vocab
+
+    def make_pool(self, capacity: int) -> DevicePagePool:
+        return DevicePagePool(capacity)
+
+    def runtime(self, pool, max_slots: int, logical_cap: int) -> StepRuntime:
+        return StepRuntime(self, pool, max_slots, logical_cap)
+
+    def plan_attention(self, sd, slot, m, n, row_off) -> None:
+        sd.segs.append((slot, m, n, row_off))
+
+    def _forward(self, n, positions, table, pool):
+        for p in positions:
+            if p >= self.position_limit:
+                raise PositionOverflow(int(p), self.position_limit)
+        table.append(pool.alloc(table.request_id, n))
+        return None
+
+    def prefill(self, tokens, positions, table, pool):
+        if not tokens:
+            raise EmptyExtend("nothing to prefill")
+        return self._forward(len(tokens), positions, table, pool)
+
+    def extend(self, tokens, start_position, table, pool):
+        if not tokens:
+            raise EmptyExtend("nothing to extend")
+        return self._forward(len(tokens), range(start_position, start_position + len(tokens)),
+                             table, pool)
+
+    def decode_step(self, last_token, position, table, pool):
+        return self._forward(1, [position], table, pool)
+
+
+def sample(logits, mask) -> int:
+    """Greedy pick among admitted ids, lowest id on ties (model.py:186-192)."""
+    logits = np.asarray(logits)
+    if hasattr(mask, "as_array"):
+        allowed = mask.as_array(len(logits))
+    else:
+        allowed = np.zeros(len(logits), dtype=bool)
+        allowed[list(mask)] = True
+    if not allowed.any():
+        raise EmptyMask("no admissible token")
+    return int(np.argmax(np.where(allowed, logits, -np.inf)))

@@ -21,7 +21,7 @@ class StepDesc:
     """Accumulates one step's records and packs them into an int32 array."""
 
     __slots__ = ("new", "segs", "dec", "ext", "jobs", "spans", "ops", "phase_starts", "last",
-                 "n_rows", "_last_kind")
+                 "n_rows", "_last_kind", "offsets")
 
     def __init__(self):
         self.new: list = []      # (slot, logical_idx, token, row, live_idx)
@@ -30,20 +30,22 @@ class StepDesc:
         self.ext: list = []      # (row_off, slot, m, n, q0)
         self.jobs: list = []     # (slot, old_len, s, reencode_from, span_off, n_spans, out_row, keep)
         self.spans: list = []    # start, end (flattened pairs)
-        self.ops: list = []      # (kind, slot, table_off, count, sp_before)
+        self.ops: list = []      # (kind, slot, table_off, count, sp_before, owner)
         self.phase_starts: list = []
         self.last: list = []     # rows whose logits are produced
         self.n_rows = 0
         self._last_kind = -1
+        self.offsets: dict = {}
 
     # ------------------------------------------------------------- page ops
-    def op(self, kind: int, slot: int, table_off: int, count: int, sp_before: int) -> None:
+    def op(self, kind: int, slot: int, table_off: int, count: int, sp_before: int,
+           owner: int) -> None:
         if count <= 0:
             return
         if kind != self._last_kind:
             self.phase_starts.append(len(self.ops))
             self._last_kind = kind
-        self.ops.append((kind, slot, table_off, count, sp_before))
+        self.ops.append((kind, slot, table_off, count, sp_before, owner))
 
     def job(self, slot, old_len, s, reencode_from, spans, out_row, keep) -> None:
         off = len(self.spans) // 2
@@ -92,6 +94,7 @@ class StepDesc:
             n_jobs=len(self.jobs), n_ops=len(self.ops), n_phases=len(self.phase_starts),
             n_last=len(self.last), dec_total=int(prefix[-1]),
         )
+        self.offsets = hdr
         head = np.zeros(L.HEADER_INTS, dtype=np.int32)
         for i, k in enumerate(_HDR):
             head[i] = hdr[k]

@@ -1,0 +1,335 @@
+"""Engine + device paging/pruning parity with the reference (GPU).
+
+The golden runs were produced by the reference Engine with ScriptedModel
+(oracle/gen_golden.py); here the B200 Engine replays the same traces and must
+reproduce, step by step, the reports, every request's live/pending lengths,
+the device block tables (CRC of the page ids) and the device free stack —
+bit-exact — plus eviction logs, applied spans and metrics.
+"""
+
+import gzip
+import json
+import zlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2507_16784_b200 as tr
+from oracle import model as om
+from oracle import paging as op
+from oracle import pruning as opr
+
+pytestmark = pytest.mark.gpu
+
+
+def _load(golden, name):
+    with gzip.open(golden / name, "rt", encoding="utf-8") as f:
+        return json.load(f)
+
+
+def crc(ids):
+    return zlib.crc32(np.asarray(ids, dtype=np.int32).tobytes())
+
+
+def _engine_for(scen, backend=None):
+    cfg = dict(scen["config"])
+    P = scen["position_limit"]
+    bc = tr.BatchConfig(**cfg, check_device=True)
+    eng = tr.Engine(backend or tr.ScriptedModel(position_limit=P), bc)
+    rids = []
+    for i, t in enumerate(scen["traces"]):
+        th = None if scen["thresholds"] is None else scen["thresholds"][i]
+        rids.append(eng.submit(scen["prompts"][i], [tr.ToolSpec(n) for n in t["tool_names"]],
+                               script=t["script"],
+                               tool_responses={int(k): v for k, v in t["tool_responses"].items()} or None,
+                               threshold=th, subsume=scen["subsume"]))
+    return eng, rids
+
+
+def test_engine_matches_reference_runs(golden):
+    scens = _load(golden, "engine_runs.json.gz")
+    for scen in scens:
+        eng, rids = _engine_for(scen)
+        assert rids == scen["rids"]
+        for i, gs in enumerate(scen["steps"]):
+            rep = eng.step()
+            where = (scen["name"], i)
+            assert [rep.step, rep.active, rep.awaiting_tool, rep.finished, rep.failed,
+                    rep.pages_free, rep.flops_units] == gs["report"], where
+            assert rep.request_live == gs["request_live"], where
+            assert rep.decoded == gs["decoded"], where
+            for rid, g in gs["reqs"].items():
+                r = eng.requests[rid]
+                pages = r.table.pages
+                assert [r.status.value, len(r.live), len(r.pending), len(pages),
+                        r.metrics.pruned_tokens] == \
+                    [g["status"], g["live"], g["pending"], g["n_pages"], g["pruned"]], where
+                assert crc(pages) == g["crc"], where
+                if "pages" in g:
+                    assert pages == g["pages"], where
+            assert [eng.pool.free_count, crc(eng.pool.free_list)] == gs["free"], where
+        assert eng.all_terminal()
+        for rid, g in scen["requests"].items():
+            r = eng.requests[rid]
+            assert [[s.start, s.end] for s in r.eviction_log] == g["eviction_log"]
+            assert [[s.start, s.end] for s in r.applied_spans] == g["applied_spans"]
+            assert r.logical == g["logical"]
+            assert r.transitions == g["transitions"], (scen["name"], rid)
+            res, mine = g["result"], eng.result(rid)
+            assert mine["status"] == res["status"]
+            for k in ("output_len", "max_cache", "position_high_water", "tool_calls",
+                      "pruned_tokens"):
+                assert mine["metrics"][k] == res["metrics"][k], (scen["name"], rid, k)
+            if res["status"] == "finished":
+                assert mine["text"] == res["text"]
+                assert mine["answer"] == res["answer"]
+            else:
+                assert mine["failure"].split(":")[0] == res["failure"].split(":")[0]
+        assert eng.pool.free_count == eng.pool.capacity
+        assert eng.pool.allocated == {}
+
+
+# ------------------------------------------------------------ numeric path
+C1 = dict(layers=2, heads=4, head_dim=32, vocab=512, position_limit=2048)
+
+
+def _rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / np.abs(np.asarray(b)).max())
+
+
+def test_backend_protocol_matches_reference_fp32(golden):
+    ref = np.load(golden / "model_ref.npz")
+    for tag, cfg in (("d16", {}), ("c1", C1)):
+        m = tr.B200Transformer(tr.ModelConfig(**cfg))
+        seq = [3, 99, 260, 45, 7, 123, 264, 10, 11, 500]
+        pool, t = m.make_pool(64), tr.PageTable("t")
+        logits = m.prefill(seq, list(range(len(seq))), t, pool)
+        k, v = tr.gather(pool, t)
+        assert _rel(logits, ref[f"{tag}_prefill_logits"]) < 1e-5
+        assert _rel(k, ref[f"{tag}_prefill_k"]) < 1e-5
+        assert _rel(v, ref[f"{tag}_prefill_v"]) < 1e-5
+        seq6 = [5, 6, 7, 8, 9, 10]
+        pool, t = m.make_pool(64), tr.PageTable("t")
+        m.prefill(seq6, list(range(6)), t, pool)
+        pool.free(t.truncate_from(1))
+        lg = m.extend(seq6[3:], 1, t, pool)
+        k, v = tr.gather(pool, t)
+        assert _rel(lg, ref[f"{tag}_reencode_logits"]) < 1e-5
+        assert _rel(k, ref[f"{tag}_reencode_k"]) < 1e-5
+        assert _rel(v, ref[f"{tag}_reencode_v"]) < 1e-5
+
+
+def test_incremental_matches_batch_and_rope_positions():
+    """tests/test_model.py:62-83 restated on the device backend."""
+    m = tr.B200Transformer(tr.ModelConfig())
+    seq = [3, 99, 260, 45, 7, 123]
+    pb, tb = m.make_pool(64), tr.PageTable("b")
+    lb = m.prefill(seq, list(range(6)), tb, pb)
+    pi, ti = m.make_pool(64), tr.PageTable("i")
+    li = m.prefill(seq[:1], [0], ti, pi)
+    for i, t in enumerate(seq[1:], start=1):
+        li = m.decode_step(t, i, ti, pi)
+    kb, vb = tr.gather(pb, tb)
+    ki, vi = tr.gather(pi, ti)
+    assert _rel(ki, kb) < 1e-5 and _rel(vi, vb) < 1e-5 and _rel(li, lb) < 1e-5
+    pool, ta = m.make_pool(64), tr.PageTable("a")
+    m.prefill([42], [0], ta, pool)
+    tb2 = tr.PageTable("u")
+    m.prefill([42], [3], tb2, pool)
+    ka, _ = tr.gather(pool, ta)
+    kb2, _ = tr.gather(pool, tb2)
+    assert np.abs(ka - kb2).max() > 1e-3
+    with pytest.raises(tr.PositionOverflow):
+        m.decode_step(1, m.position_limit, ta, pool)
+
+
+def test_engine_numeric_replay_matches_reference(golden):
+    """C1 fp32 replay of deep(3,2) prompt "p:" T=1 through the batched engine:
+    every step's logits and the post-prune working memory match the reference."""
+    ref = np.load(golden / "model_ref.npz")
+    recs = {tuple(r["gen"]): r for r in _load(golden, "events.json.gz")}
+    rec = recs[("deep_recursion_tree", 3, 2, 0)]
+    eng = tr.Engine(tr.B200Transformer(tr.ModelConfig(**C1)),
+                    tr.BatchConfig(buffer_threshold=1, position_limit=2048, pool_pages=4096,
+                                   check_device=True))
+    rid = eng.submit("p:", [], script=rec["script"])
+    req = eng.requests[rid]
+    logits, kv_after = [], None
+    while not eng.all_terminal():
+        eng.step()
+        if req.last_logits is not None and req.status.value == "decoding":
+            logits.append(np.asarray(req.last_logits))
+        if req.metrics.pruned_tokens and kv_after is None and req.status.value == "decoding":
+            kv_after = tr.gather(eng.pool, req.table)
+    got = np.stack(logits)
+    want = ref["c1_replay_logits"]
+    assert got.shape == want.shape
+    assert _rel(got, want) < 1e-5
+    assert _rel(kv_after[0], ref["c1_replay_k_after_prune"]) < 1e-5
+    assert _rel(kv_after[1], ref["c1_replay_v_after_prune"]) < 1e-5
+
+
+def _kv_equivalence(eng, req, model, rtol, greedy_steps=8):
+    """verify.py:99-135 restated: working memory == fresh prefill of live tokens."""
+    live_tokens = [req.logical[i] for i in req.live]
+    n = len(live_tokens)
+    scratch = model.make_pool(n + greedy_steps + 2)
+    ot = tr.PageTable("oracle")
+    o_logits = model.prefill(live_tokens, list(range(n)), ot, scratch)
+    kr, vr = tr.gather(eng.pool, req.table)
+    ko, vo = tr.gather(scratch, ot)
+    assert _rel(kr, ko) < rtol and _rel(vr, vo) < rtol
+    return max(_rel(kr, ko), _rel(vr, vo))
+
+
+@pytest.mark.parametrize("threshold", [0, 1, 2])
+def test_prune_reencode_equals_fresh_prefill(golden, threshold):
+    """Acceptance criterion 1 (tests/test_acceptance.py:40-53) on the device:
+    after every eviction + re-encode the retained working memory equals a fresh
+    prefill of the pruned logical sequence at 1e-5 (fp32)."""
+    recs = [r for r in _load(golden, "events.json.gz") if r["gen"][0] == "random_tree"][:25]
+    model = tr.B200Transformer(tr.ModelConfig(**C1))
+    checked = 0
+    for rec in recs:
+        eng = tr.Engine(model, tr.BatchConfig(buffer_threshold=threshold, position_limit=2048,
+                                              pool_pages=8192))
+        rid = eng.submit("task:", [tr.ToolSpec(n) for n in rec["tool_names"]], script=rec["script"],
+                         tool_responses={int(k): v for k, v in rec["tool_responses"].items()} or None)
+        req = eng.requests[rid]
+        pruned = 0
+        while not eng.all_terminal():
+            eng.step()
+            if req.metrics.pruned_tokens > pruned and req.status.value == "decoding":
+                pruned = req.metrics.pruned_tokens
+                _kv_equivalence(eng, req, model, 1e-5)
+                checked += 1
+        assert eng.result(rid)["text"] == rec["text"]
+    assert checked >= 10
+
+
+def test_batched_engine_equals_sequential_oracle_bf16(golden):
+    """Qwen3-shaped GQA (32q/8kv, D=128) bf16: the batched engine's K/V and
+    logits vs the fp32 oracle model run per request (same bf16-rounded weights)."""
+    from paper_2507_16784_b200.traces import load_corpus, make_trace_from_text
+    cfg = tr.ModelConfig(layers=2, heads=32, kv_heads=8, head_dim=128, mlp_dim=1024, vocab=512,
+                         position_limit=4096, precision="bfloat16", rope_base=1e6)
+    model = tr.B200Transformer(cfg)
+    docs = load_corpus(golden / "corpus_tool_chain32.json.gz")[:6]
+    traces = [make_trace_from_text(d) for d in docs]
+    eng = tr.Engine(model, tr.BatchConfig(max_batch=6, buffer_threshold=2, position_limit=4096,
+                                          pool_pages=20000, check_masks=False))
+    rids = [eng.submit(f"q{i}:", [tr.ToolSpec(n) for n in t.tool_names], script=t.script,
+                       tool_responses=t.tool_responses) for i, t in enumerate(traces)]
+    # oracle weights: the device weights upcast
+    w = {"emb": model.emb.float().cpu().numpy(), "layers": [],
+         "inv_freq": (1e6 ** (-np.arange(64) / 64)).astype(np.float32)}
+    dm, hq, hkv, D = 4096, 32, 8, 128
+    for li in range(cfg.layers):
+        wqkv = model.wqkv[li].float().cpu().numpy()
+        w["layers"].append({"wq": wqkv[:, :hq * D], "wk": wqkv[:, hq * D:(hq + hkv) * D],
+                            "wv": wqkv[:, (hq + hkv) * D:], "wo": model.wo[li].float().cpu().numpy(),
+                            "w1": model.w1[li].float().cpu().numpy(),
+                            "w2": model.w2[li].float().cpu().numpy()})
+    ocfg = om.Config(layers=2, heads=32, kv_heads=8, head_dim=128, mlp_dim=1024, vocab=512,
+                     position_limit=4096, rope_base=1e6)
+    oracle = om.Model(ocfg, w)
+    checks = 0
+    for step in range(400):
+        eng.step()
+        if step % 97 != 96:
+            continue
+        for rid in rids:
+            req = eng.requests[rid]
+            if req.status.value != "decoding" or not req.live:
+                continue
+            toks = [req.logical[i] for i in req.live]
+            pool, t = oracle.make_pool(len(toks) + 1), op.PageTable("o")
+            lo = oracle.prefill(toks, list(range(len(toks))), t, pool)
+            ko, vo = op.gather(pool, t)
+            kr, vr = tr.gather(eng.pool, req.table)
+            assert np.abs(kr - ko).max() < 0.1 and np.abs(vr - vo).max() < 0.1
+            assert np.abs(kr - ko).mean() < 5e-3
+            checks += 1
+    assert checks >= 6
+
+
+# ---------------------------------------------------- reference API parity
+def test_pool_api_semantics():
+    """tests/test_paging.py:9-71 on the device pool."""
+    pool = tr.PagePool(8)
+    assert pool.alloc("r", 0) == [] and pool.free_count == 8
+    ids = pool.alloc("r", 5)
+    assert ids == [0, 1, 2, 3, 4] and pool.free_count == 3 and len(pool.allocated) == 5
+    pool.free(ids)
+    assert pool.free_count == 8 and not pool.allocated
+    with pytest.raises(tr.OutOfPages) as info:
+        pool.alloc("r", 9)
+    assert info.value.needed == 9 and info.value.available == 8
+    one = pool.alloc("r", 1)
+    pool.free(one)
+    with pytest.raises(tr.DoubleFree):
+        pool.free(one)
+    p4 = tr.PagePool(4)
+    p4.alloc("a", 1)
+    p4.alloc("b", 2)
+    assert p4.snapshot() == {"capacity": 4, "free": 1, "allocated": 3,
+                             "per_request": {"a": {"live_tokens": 1}, "b": {"live_tokens": 2}}}
+
+
+def test_pool_random_interleavings_match_oracle():
+    import random
+    rng = random.Random(0)
+    pool, ref = tr.PagePool(64), op.PagePool(64)
+    held: dict = {}
+    for _ in range(300):
+        rid = f"r{rng.randrange(6)}"
+        if rng.random() < 0.55:
+            n = rng.randrange(0, 5)
+            if n <= ref.free_count:
+                a = pool.alloc(rid, n)
+                assert a == ref.alloc(rid, n)
+                held.setdefault(rid, []).extend(a)
+        elif held.get(rid):
+            k = rng.randrange(1, len(held[rid]) + 1)
+            pool.free(held[rid][:k])
+            ref.free(held[rid][:k])
+            del held[rid][:k]
+        assert pool.free_count == ref.free_count
+    assert pool.free_list == ref.free_list
+    assert pool.allocated == ref.allocated
+
+
+def test_apply_device_matches_reference_cases():
+    """tests/test_pruning.py:107-157 through the device K4 kernel."""
+    pool = tr.PagePool(32)
+    t = tr.PageTable("r")
+    t.append(pool.alloc("r", 6))
+    freed, suffix, start, new_live = tr.apply(tr.PrunePlan([tr.TokenSpan(1, 3)], 1, 2), t,
+                                              list(range(6)), [101, 111, 112, 102, 121, 999])
+    assert len(freed) == 5 and suffix == [102, 121, 999] and start == 1
+    assert new_live == [0, 3, 4, 5] and len(t) == 1
+    t = tr.PageTable("q")
+    t.append(list(range(10)))
+    live = [0, 1, 2, 3, 6, 7, 8, 9, 10, 11]
+    _, suffix, start, new_live = tr.apply(tr.PrunePlan([tr.TokenSpan(2, 9)], 2, 7), t, live,
+                                          list(range(12)))
+    assert new_live == [0, 1, 9, 10, 11] and suffix == [9, 10, 11] and start == 2
+    with pytest.raises(tr.SpanOutOfRange):
+        t = tr.PageTable("x")
+        t.append([0, 1, 2, 3])
+        tr.apply(tr.PrunePlan([tr.TokenSpan(2, 9)], 2, 7), t, [0, 1, 2, 3], [1, 2, 3, 4])
+    import random
+    rng = random.Random(3)
+    for _ in range(40):
+        n = rng.randrange(8, 40)
+        tokens = [rng.randrange(500) for _ in range(n)]
+        t = tr.PageTable("z")
+        t.append(list(range(n)))
+        a = rng.randrange(0, n - 2)
+        b = a + rng.randrange(1, n - a)
+        _, suffix, start, new_live = tr.apply(tr.PrunePlan([tr.TokenSpan(a, b)], a, b - a), t,
+                                              list(range(n)), tokens)
+        assert new_live == opr.surgery(list(range(n)), [opr.Span(a, b)])
+        assert suffix == [tokens[i] for i in new_live[start:]]

@@ -216,13 +216,13 @@ def test_page_ops_match_lifo_oracle():
                 sp = pool.free_count
                 off = len(t)
                 t.append(pool.alloc(s, nn))
-                sd.op(L.OP_ALLOC, s, off, nn, sp)
+                sd.op(L.OP_ALLOC, s, off, nn, sp, s)
             elif len(t):
                 cut = int(rng.integers(0, len(t)))
                 sp = pool.free_count
                 freed = t.truncate_from(cut)
                 pool.free(freed)
-                sd.op(L.OP_FREE, s, cut, len(freed), sp)
+                sd.op(L.OP_FREE, s, cut, len(freed), sp, s)
         step = _dev(sd.pack())
         L.call("tim_page_ops", _ptr(step), _ptr(stack), _ptr(owner), cap, _ptr(tab_d), stride,
                _ptr(err), _stream())

@@ -104,6 +104,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def reduce_over_ranks(dist, times, counts, device="cpu"):
+    """Times: max over ranks (the job ends with its slowest rank); counts: sum."""
+    import torch
+    if dist is None:
+        return (*times, *counts)
+    t = torch.tensor(times, dtype=torch.float64, device=device)
+    c = torch.tensor(counts, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(c, op=dist.ReduceOp.SUM)
+    return (*[float(x) for x in t], *[float(x) for x in c])
+
+
 # --------------------------------------------------------------------- GPU arm
 def build_engine(rank: int, n_req: int, threshold: int):
     import paper_2507_16784_b200 as tr
@@ -196,15 +208,11 @@ def run_gpu(args, rank: int, world: int, dist):
     e2e_ms = f0.elapsed_time(f1)
     wall_ms = (time.perf_counter() - w0) * 1000.0
 
-    vals = torch.tensor([ms, e2e_ms, planned_tokens, e2e_tokens, attn_ms, attn_bytes, launches],
-                        dtype=torch.float64, device="cuda")
-    if dist is not None:
-        mx = vals.clone()
-        sm = vals.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms, e2e_ms = float(mx[0]), float(mx[1])
-        planned_tokens, e2e_tokens = float(sm[2]), float(sm[3])
+    print(f"[rank {rank}] value window: {planned_tokens} tokens in {ms:.1f} ms; e2e window: "
+          f"{e2e_tokens} tokens in {e2e_ms:.1f} ms GPU / {wall_ms:.1f} ms wall; "
+          f"graphs={len(rt.graphs)} launches={launches}", file=sys.stderr)
+    ms, e2e_ms, planned_tokens, e2e_tokens = reduce_over_ranks(
+        dist, [ms, e2e_ms], [planned_tokens, e2e_tokens], device="cuda")
     return dict(ms=ms, e2e_ms=e2e_ms, wall_ms=wall_ms, tokens=planned_tokens, e2e_tokens=e2e_tokens,
                 attn_ms=attn_ms, attn_bytes=attn_bytes, launches=launches, clocks=clk,
                 h2d=h2d / args.steps, d2h=d2h / args.steps, mean_live=mean_live,

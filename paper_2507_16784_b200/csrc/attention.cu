@@ -25,6 +25,9 @@
 namespace tim {
 
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kMaxHeads = 128;      // hq bound for the in-kernel combine
+constexpr int kCombineChunk = 8;    // partials merged per smem pass
+constexpr int kIdChunk = 1024;      // page ids staged per producer refill (multiple of TK)
 
 // ===================================================================== K1
 template <int D, int HKV>
@@ -36,7 +39,7 @@ struct DecCfg {
   static constexpr int STAGES_RAW = 204800 / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
   static constexpr int THREADS = (HKV + 1) * 32;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 128;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 16 + kIdChunk * 4;
   static constexpr int KC = D / 16;
   static constexpr int NT = D / 8;
 };
@@ -57,6 +60,8 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
   int* sflag = reinterpret_cast<int*>(empty + C::STAGES);
+  __shared__ float s_m[kMaxHeads], s_inv[kMaxHeads];
+  __shared__ float s_w[kCombineChunk][kMaxHeads];
 
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
   const int n_dec = hd.n_dec;
@@ -92,24 +97,34 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
 
   if (warp == HKV) {
     // ------------------------------------------------------------ producer
+    // Page ids of the piece are staged into shared memory a chunk at a time
+    // (one coalesced read per kIdChunk tokens), so the id latency is off the
+    // per-stage critical path; each stage is then 2*TK bulk copies.
+    int32_t* s_ids = reinterpret_cast<int32_t*>(sflag + 4);
     int it = 0;
     for (int r = r0; r < n_dec && prefix[r] < end; ++r) {
       const int64_t lo = prefix[r], hi = prefix[r + 1];
       const int p0 = (int)((start > lo ? start : lo) - lo);
       const int p1 = (int)((end < hi ? end : hi) - lo);
       const int32_t* trow = tables + (int64_t)dec[r * TIM_DEC_FIELDS + 1] * tstride;
-      for (int k0 = p0; k0 < p1; k0 += C::TK, ++it) {
-        const int ntok = (p1 - k0) < C::TK ? (p1 - k0) : C::TK;
-        const int stg = it % C::STAGES;
-        if (it >= C::STAGES) mbar_wait(&empty[stg], ((it / C::STAGES) & 1) ^ 1);
-        if (lane == 0) mbar_arrive_expect_tx(&full[stg], 2 * C::TK * C::ROW_BYTES);
+      for (int c0 = p0; c0 < p1; c0 += kIdChunk) {
+        const int c1 = (p1 - c0) < kIdChunk ? p1 : c0 + kIdChunk;
         __syncwarp();
-        const int row = lane & (C::TK - 1);
-        const int tok = k0 + (row < ntok ? row : ntok - 1);  // pad rows duplicate a valid row
-        const int32_t page = trow[tok];
-        uint8_t* base = smem + stg * C::STAGE_BYTES + (lane >= C::TK ? C::TK * C::ROW_STRIDE : 0);
-        const __nv_bfloat16* src = (lane >= C::TK ? vl : kl) + (int64_t)page * (HKV * D);
-        bulk_g2s(base + row * C::ROW_STRIDE, src, C::ROW_BYTES, &full[stg]);
+#pragma unroll 8
+        for (int i = lane; i < c1 - c0; i += 32) s_ids[i] = __ldg(trow + c0 + i);
+        __syncwarp();
+        for (int k0 = c0; k0 < c1; k0 += C::TK, ++it) {
+          const int ntok = (c1 - k0) < C::TK ? (c1 - k0) : C::TK;
+          const int stg = it % C::STAGES;
+          if (it >= C::STAGES) mbar_wait(&empty[stg], ((it / C::STAGES) & 1) ^ 1);
+          if (lane == 0) mbar_arrive_expect_tx(&full[stg], 2 * C::TK * C::ROW_BYTES);
+          __syncwarp();
+          const int row = lane & (C::TK - 1);
+          const int32_t page = s_ids[k0 - c0 + (row < ntok ? row : ntok - 1)];  // pad rows repeat a valid row
+          uint8_t* base = smem + stg * C::STAGE_BYTES + (lane >= C::TK ? C::TK * C::ROW_STRIDE : 0);
+          const __nv_bfloat16* src = (lane >= C::TK ? vl : kl) + (int64_t)page * (HKV * D);
+          bulk_g2s(base + row * C::ROW_STRIDE, src, C::ROW_BYTES, &full[stg]);
+        }
       }
     }
     return;
@@ -268,20 +283,60 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
     asm volatile("bar.sync 1, %0;" ::"n"(HKV * 32));
     if (*sflag) {
       __threadfence();
-      // K6: log-sum-exp merge of this query's partials (slots c' + r)
-      for (int e = threadIdx.x; e < hq * D; e += HKV * 32) {
-        const int head = e / D;
+      // K6: log-sum-exp merge of this query's partials (slots c' + r).  Per
+      // head: M = max m_p, weight_p = exp2(m_p - M) / sum_q exp2(m_q - M) l_q;
+      // then every thread merges float4 slices of the hq*D outputs.
+      const int nthr = HKV * 32;
+      for (int h = threadIdx.x; h < hq; h += nthr) {
         float M = -INFINITY;
         for (int64_t cc = c_first; cc <= c_last; ++cc)
-          M = fmaxf(M, __ldcg(ws_ml + ((cc + r) * hq + head) * 2));
-        float num = 0.f, den = 0.f;
+          M = fmaxf(M, __ldcg(ws_ml + ((cc + r) * hq + h) * 2));
+        float den = 0.f;
         for (int64_t cc = c_first; cc <= c_last; ++cc) {
-          const float2 ml = __ldcg(reinterpret_cast<const float2*>(ws_ml + ((cc + r) * hq + head) * 2));
-          const float w = ml.x == -INFINITY ? 0.f : fast_exp2(ml.x - M);
-          num += w * __ldcg(ws_o + ((cc + r) * hq) * D + e);
-          den += w * ml.y;
+          const float2 ml = __ldcg(reinterpret_cast<const float2*>(ws_ml + ((cc + r) * hq + h) * 2));
+          den += (ml.x == -INFINITY ? 0.f : fast_exp2(ml.x - M)) * ml.y;
         }
-        out[(int64_t)qrow * hq * D + e] = __float2bfloat16_rn(num / den);
+        s_m[h] = M;
+        s_inv[h] = 1.f / den;
+      }
+      constexpr int V4 = 4;  // float4 slices per thread per pass
+      const int n4 = hq * D / 4;
+      for (int base = 0; base < n4; base += nthr * V4) {
+        float4 acc[V4];
+#pragma unroll
+        for (int k = 0; k < V4; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t c0 = c_first; c0 <= c_last; c0 += kCombineChunk) {
+          const int np = (int)((c_last - c0 + 1) < kCombineChunk ? (c_last - c0 + 1) : kCombineChunk);
+          asm volatile("bar.sync 1, %0;" ::"n"(HKV * 32));
+          for (int i = threadIdx.x; i < np * hq; i += nthr) {
+            const int pp = i / hq, h = i - pp * hq;
+            const float mm = __ldcg(ws_ml + ((c0 + pp + r) * hq + h) * 2);
+            s_w[pp][h] = mm == -INFINITY ? 0.f : fast_exp2(mm - s_m[h]) * s_inv[h];
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(HKV * 32));
+          for (int pp = 0; pp < np; ++pp) {
+            const float4* src = reinterpret_cast<const float4*>(ws_o + (c0 + pp + r) * hq * D);
+#pragma unroll
+            for (int k = 0; k < V4; ++k) {
+              const int e4 = base + threadIdx.x + k * nthr;
+              if (e4 < n4) {
+                const float w = s_w[pp][(e4 * 4) / D];
+                const float4 v = __ldcg(src + e4);
+                acc[k].x += w * v.x; acc[k].y += w * v.y; acc[k].z += w * v.z; acc[k].w += w * v.w;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < V4; ++k) {
+          const int e4 = base + threadIdx.x + k * nthr;
+          if (e4 < n4) {
+            uint2 pk;
+            pk.x = pack_bf16(acc[k].x, acc[k].y);
+            pk.y = pack_bf16(acc[k].z, acc[k].w);
+            *reinterpret_cast<uint2*>(out + (int64_t)qrow * hq * D + e4 * 4) = pk;
+          }
+        }
       }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(HKV * 32));

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import json
 import math
+import os
 from dataclasses import asdict, dataclass
 from pathlib import Path
 
@@ -161,6 +162,11 @@ class StepRuntime:
         self.last_logits = None
         self.launches = 0
         self._last_upload_bytes = 0
+        self.use_graphs = (model is not None and getattr(model, "has_weights", False) and max_slots > 0
+                           and os.environ.get("TIMRUN_GRAPHS", "1") != "0")
+        self.graphs: dict = {}
+        self.graph_pool = None
+        self.gstep = None
         self.recording = None        # list -> record descriptors instead of executing
         self.attn_events = None      # list -> CUDA events around layer-0 decode attention
 
@@ -169,6 +175,9 @@ class StepRuntime:
         if n <= self._rows:
             return
         R = 1 << max(6, (n - 1).bit_length())
+        if self.use_graphs:
+            R = max(R, self.GRAPH_BUCKETS[-1])
+            self.graphs = {}          # captured graphs point at the old buffers
         d = self.dev
         self.row_tokens = torch.zeros(R, dtype=torch.int32, device=d)
         self.row_pages = torch.full((R,), -1, dtype=torch.int32, device=d)
@@ -200,15 +209,35 @@ class StepRuntime:
         ev = torch.cuda.Event()
         ev.record()
         self._ring_ev[i] = ev
-        return self.step_dev
+        return self.step_dev[:n]
 
     # -------------------------------------------------------------- step
+    GRAPH_BUCKETS = (64, 128, 256, 512, 1024)
+
+    def graph_bucket(self, n_rows: int):
+        if not self.use_graphs:
+            return None
+        for b in self.GRAPH_BUCKETS:
+            if n_rows <= b:
+                return b
+        return None
+
     def run_step(self, sd: StepDesc, forward: bool = True):
         """Execute one planned step; returns the greedy tokens of sd.last rows
         (device tensor) or None when there is nothing to encode.  In record
         mode the packed descriptor is only stored (see replay)."""
+        b = self.graph_bucket(sd.n_rows) if forward and sd.n_rows else None
+        if b is not None:
+            sd.rows_pad = b
+            sd.last_pad = self.max_slots
         arr = sd.pack()
-        self._ensure_rows(max(sd.n_rows, 1))
+        self._ensure_rows(max(sd.rows_pad or sd.n_rows, 1))
+        if self.gstep is None or self.gstep.numel() < arr.size:
+            if self.use_graphs:
+                self.gstep = torch.zeros(max(1 << 16, 1 << (arr.size - 1).bit_length()),
+                                         dtype=torch.int32, device=self.dev)
+                self.graphs = {}
+                self.graph_pool = torch.cuda.graph_pool_handle()
         if self.recording is not None:
             self.recording.append((sd, arr, forward))
             return None
@@ -398,69 +427,145 @@ class B200Transformer:
         rt.ws = torch.zeros(L.load().tim_decode_ws_floats(n_ctas, R, cfg.heads, D), device=d)
         rt.counters = torch.zeros(R, dtype=torch.int32, device=d)
 
-    def forward_rows(self, rt: StepRuntime, step: torch.Tensor, sd: StepDesc):
-        """The batched forward over staged rows (model.py:137-164 for every segment)."""
-        cfg = self.config
-        T = sd.n_rows
-        st = stream_handle()
-        td = cfg.tim_dtype
-        dm, D, hq, hkv = cfg.model_dim, cfg.head_dim, cfg.heads, cfg.n_kv
-        h, x, qkv, q, ctx, u = rt.h[:T], rt.x[:T], rt.qkv[:T], rt.q, rt.ctx[:T], rt.u[:T]
-        sp = step.data_ptr()
+    # The forward is split in three phases so that a decode step can run as
+    # two captured CUDA graphs around one eagerly launched layer-0 attention
+    # (which bench.py brackets with CUDA events for the live roofline figure).
+    def _pre(self, rt: StepRuntime, sp: int, T: int) -> int:
+        cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
+        dm = cfg.model_dim
+        h = rt.h[:T]
         L.call("tim_embed", rt.row_tokens.data_ptr(), T, self.emb.data_ptr(), dm, h.data_ptr(), td, st)
+        return 1 + self._layer_head(rt, 0, T)
+
+    def _layer_head(self, rt, li, T) -> int:
+        cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
+        dm, D = cfg.model_dim, cfg.head_dim
+        L.call("tim_rmsnorm", rt.h.data_ptr(), dm, rt.x.data_ptr(), dm, T, dm, 1e-6, td, st)
+        torch.matmul(rt.x[:T], self.wqkv[li], out=rt.qkv[:T])
+        L.call("tim_rope_kv_store", rt.qkv.data_ptr(), T, rt.row_pos.data_ptr(), rt.row_pages.data_ptr(),
+               self.cos.data_ptr(), self.sin.data_ptr(), cfg.heads, cfg.n_kv, D, rt.q.data_ptr(),
+               self.pool_layer(rt.pool.K_layers, li), self.pool_layer(rt.pool.V_layers, li), td, st)
+        return 2
+
+    def _attn(self, rt, sp: int, li: int, T: int, has_dec: bool, has_ext: bool, max_ext: int,
+              timed=None) -> int:
+        cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
+        D, hq, hkv = cfg.head_dim, cfg.heads, cfg.n_kv
+        kl = self.pool_layer(rt.pool.K_layers, li)
+        vl = self.pool_layer(rt.pool.V_layers, li)
         tstride = rt.tables.shape[1]
-        launches = 1
-        for li in range(cfg.layers):
-            kl = self.pool_layer(rt.pool.K_layers, li)
-            vl = self.pool_layer(rt.pool.V_layers, li)
-            L.call("tim_rmsnorm", h.data_ptr(), dm, x.data_ptr(), dm, T, dm, 1e-6, td, st)
-            torch.matmul(x, self.wqkv[li], out=qkv)
-            L.call("tim_rope_kv_store", qkv.data_ptr(), T, rt.row_pos.data_ptr(),
-                   rt.row_pages.data_ptr(), self.cos.data_ptr(), self.sin.data_ptr(), hq, hkv, D,
-                   q.data_ptr(), kl, vl, td, st)
-            launches += 2
-            if self.tensor_cores:
-                if sd.dec:
-                    timed = li == 0 and rt.attn_events is not None
-                    if timed:
-                        e0 = torch.cuda.Event(enable_timing=True)
-                        e0.record()
-                    L.call("tim_attn_decode", sp, q.data_ptr(), ctx.data_ptr(), kl, vl,
-                           rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, rt.ws.data_ptr(),
-                           rt.counters.data_ptr(), rt.n_ctas, rt.max_dec, td, st)
-                    launches += 1
-                    if timed:
-                        e1 = torch.cuda.Event(enable_timing=True)
-                        e1.record()
-                        rt.attn_events.append((e0, e1, sd))
-                if sd.ext:
-                    L.call("tim_attn_extend", sp, len(sd.ext), q.data_ptr(), ctx.data_ptr(), kl, vl,
-                           rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, td, st)
-                    launches += 1
-            else:
-                L.call("tim_attn_extend", sp, T, q.data_ptr(), ctx.data_ptr(), kl, vl,
-                       rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, td, st)
-                launches += 1
-            h.addmm_(ctx, self.wo[li])
-            L.call("tim_rmsnorm", h.data_ptr(), dm, x.data_ptr(), dm, T, dm, 1e-6, td, st)
-            torch.matmul(x, self.w1[li], out=u)
-            L.call("tim_silu", u.data_ptr(), u.numel(), td, st)
-            h.addmm_(u, self.w2[li])
-            launches += 2
-        n_last = len(sd.last)
-        off = sd.offsets["off_last"]
+        n = 0
+        if not self.tensor_cores:
+            L.call("tim_attn_extend", sp, T, rt.q.data_ptr(), rt.ctx.data_ptr(), kl, vl,
+                   rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, td, st)
+            return 1
+        if has_dec:
+            if timed is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            L.call("tim_attn_decode", sp, rt.q.data_ptr(), rt.ctx.data_ptr(), kl, vl,
+                   rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, rt.ws.data_ptr(),
+                   rt.counters.data_ptr(), rt.n_ctas, rt.max_dec, td, st)
+            if timed is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record()
+                timed.append((e0, e1))
+            n += 1
+        if has_ext:
+            L.call("tim_attn_extend", sp, max_ext, rt.q.data_ptr(), rt.ctx.data_ptr(), kl, vl,
+                   rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, td, st)
+            n += 1
+        return n
+
+    def _layer_tail(self, rt, li, T) -> int:
+        cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
+        dm = cfg.model_dim
+        h = rt.h[:T]
+        h.addmm_(rt.ctx[:T], self.wo[li])
+        L.call("tim_rmsnorm", rt.h.data_ptr(), dm, rt.x.data_ptr(), dm, T, dm, 1e-6, td, st)
+        u = rt.u[:T]
+        torch.matmul(rt.x[:T], self.w1[li], out=u)
+        L.call("tim_silu", u.data_ptr(), u.numel(), td, st)
+        h.addmm_(u, self.w2[li])
+        return 2
+
+    def _post(self, rt, sp: int, step: torch.Tensor, T: int, has_dec, has_ext, max_ext,
+              n_last: int):
+        cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
+        dm = cfg.model_dim
+        n = self._layer_tail(rt, 0, T)
+        for li in range(1, cfg.layers):
+            n += self._layer_head(rt, li, T)
+            n += self._attn(rt, sp, li, T, has_dec, has_ext, max_ext)
+            n += self._layer_tail(rt, li, T)
+        off = L.HEADER_INTS                     # `last` is packed first (stepdesc.pack)
         idx = step[off: off + n_last].long()
-        hl = h.index_select(0, idx)
+        hl = rt.h.index_select(0, idx)
         xl = torch.empty_like(hl)
         L.call("tim_rmsnorm", hl.data_ptr(), dm, xl.data_ptr(), dm, n_last, dm, 1e-6, td, st)
         logits = torch.matmul(xl.float(), self.emb_t32)
         toks = torch.empty(n_last, dtype=torch.int32, device=self.dev)
         L.call("tim_argmax", logits.data_ptr(), n_last, cfg.vocab, toks.data_ptr(), L.DTYPE_F32, st)
-        launches += 2
-        rt.launches += launches
+        return n + 2, logits, toks
+
+    def _max_ext(self, rt, T: int) -> int:
+        return (T + self.qpi - 1) // self.qpi + max(rt.max_slots, 1)
+
+    def forward_rows(self, rt: StepRuntime, step: torch.Tensor, sd: StepDesc):
+        """The batched forward over staged rows (model.py:137-164 for every segment).
+        Graph mode replays captured graphs keyed by (row bucket, has-extend)."""
+        has_dec, has_ext = bool(sd.dec), bool(sd.ext)
+        timed = rt.attn_events
+        if rt.graph_bucket(sd.n_rows) is not None and sd.rows_pad:
+            Tb = sd.rows_pad
+            rt.gstep[: step.numel()].copy_(step) if step.data_ptr() != rt.gstep.data_ptr() else None
+            key = (Tb, has_ext)
+            g = rt.graphs.get(key)
+            if g is None:
+                g = self._capture(rt, Tb, has_ext, sd.last_pad)
+                rt.graphs[key] = g
+            g["pre"].replay()
+            ev = [] if timed is not None else None
+            n_att = self._attn(rt, rt.gstep.data_ptr(), 0, Tb, True, has_ext,
+                               self._max_ext(rt, Tb), ev)
+            g["post"].replay()
+            rt.launches += g["launches"] + n_att
+            if ev:
+                timed.append((ev[0][0], ev[0][1], sd))
+            logits, toks = g["logits"][: len(sd.last)].clone(), g["toks"]
+        else:
+            T = sd.n_rows
+            sp = step.data_ptr()
+            n = self._pre(rt, sp, T)
+            ev = [] if timed is not None else None
+            n += self._attn(rt, sp, 0, T, has_dec, has_ext, len(sd.ext), ev)
+            if ev:
+                timed.append((ev[0][0], ev[0][1], sd))
+            m, logits, toks = self._post(rt, sp, step, T, has_dec, has_ext, len(sd.ext), len(sd.last))
+            rt.launches += n + m
         rt.last_logits = logits
         rt.last_tokens = toks
         return toks
+
+    def _capture(self, rt: StepRuntime, Tb: int, has_ext: bool, n_last: int) -> dict:
+        """Capture the pre (embed + layer-0 head) and post (rest) phases for a row
+        bucket; the descriptor is read from the fixed rt.gstep buffer."""
+        sp = rt.gstep.data_ptr()
+        mx = self._max_ext(rt, Tb)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):          # warm-up (cuBLAS handles, heuristics)
+            self._pre(rt, sp, Tb)
+            self._attn(rt, sp, 0, Tb, True, has_ext, mx)
+            self._post(rt, sp, rt.gstep, Tb, True, has_ext, mx, n_last)
+        torch.cuda.current_stream().wait_stream(side)
+        pre, post = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(pre):
+            n_pre = self._pre(rt, sp, Tb)
+        with torch.cuda.graph(post):
+            n_post, logits, toks = self._post(rt, sp, rt.gstep, Tb, True, has_ext, mx, n_last)
+        return {"pre": pre, "post": post, "logits": logits, "toks": toks,
+                "launches": n_pre + n_post}
 
     @staticmethod
     def pool_layer(t: torch.Tensor, li: int) -> int:

@@ -21,7 +21,7 @@ class StepDesc:
     """Accumulates one step's records and packs them into an int32 array."""
 
     __slots__ = ("new", "segs", "dec", "ext", "jobs", "spans", "ops", "phase_starts", "last",
-                 "n_rows", "_last_kind", "offsets")
+                 "n_rows", "_last_kind", "offsets", "rows_pad", "last_pad")
 
     def __init__(self):
         self.new: list = []      # (slot, logical_idx, token, row, live_idx)
@@ -36,6 +36,8 @@ class StepDesc:
         self.n_rows = 0
         self._last_kind = -1
         self.offsets: dict = {}
+        self.rows_pad: int | None = None   # row buffers padded to this many rows (graph bucket)
+        self.last_pad = 0                  # `last` padded to this many entries (graph bucket)
 
     # ------------------------------------------------------------- page ops
     def op(self, kind: int, slot: int, table_off: int, count: int, sp_before: int,
@@ -54,7 +56,9 @@ class StepDesc:
         self.jobs.append((slot, old_len, s, reencode_from, off, len(spans), out_row, keep))
 
     # ---------------------------------------------------------------- pack
-    def pack(self, n_rows_pad: int | None = None) -> np.ndarray:
+    def pack(self) -> np.ndarray:
+        """Header, then `last` (first, so its offset is fixed at HEADER_INTS and a
+        captured graph can index it), then the other record arrays."""
         parts = []
         off = L.HEADER_INTS
         hdr = dict.fromkeys(_HDR, 0)
@@ -68,6 +72,8 @@ class StepDesc:
             parts.append(arr)
             off += arr.size
 
+        last = list(self.last) + [0] * max(0, self.last_pad - len(self.last))
+        add("last", last, 0)
         add("new", self.new, L.NEW_FIELDS)
         add("segs", self.segs, L.SEG_FIELDS)
         add("dec", self.dec, L.DEC_FIELDS)
@@ -86,13 +92,12 @@ class StepDesc:
         hdr["off_phases"] = off
         parts.append(np.asarray(phases, dtype=np.int32))
         off += len(phases)
-        add("last", self.last, 0)
         hdr.update(
             n_rows=self.n_rows,
-            n_rows_pad=self.n_rows if n_rows_pad is None else n_rows_pad,
+            n_rows_pad=self.n_rows if self.rows_pad is None else max(self.rows_pad, self.n_rows),
             n_new=len(self.new), n_segs=len(self.segs), n_dec=len(self.dec), n_ext=len(self.ext),
             n_jobs=len(self.jobs), n_ops=len(self.ops), n_phases=len(self.phase_starts),
-            n_last=len(self.last), dec_total=int(prefix[-1]),
+            n_last=len(last), dec_total=int(prefix[-1]),
         )
         self.offsets = hdr
         head = np.zeros(L.HEADER_INTS, dtype=np.int32)

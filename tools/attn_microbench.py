@@ -1,0 +1,81 @@
+"""Decode-attention microbenchmark at the C2 shape (ncu target and quick A/B).
+
+64 requests x L retained pages (default 724, the reference's C2 mean live),
+Qwen3-8B GQA 32q/8kv, D=128, bf16, one layer.  Prints achieved algorithmic
+GB/s from CUDA events (inputs > L2 by rotating over several layers' pools).
+"""
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2507_16784_b200 import _lib as L  # noqa: E402
+from paper_2507_16784_b200.stepdesc import StepDesc  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--live", type=int, default=724)
+    ap.add_argument("--jitter", type=float, default=0.5)
+    ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--ctas", type=int, default=0)
+    a = ap.parse_args()
+    hq, hkv, d = 32, 8, 128
+    rng = np.random.default_rng(0)
+    lens = np.maximum(1, (a.live * (1 + a.jitter * (rng.random(a.batch) * 2 - 1)))).astype(int)
+    cap = int(lens.sum()) + 16
+    stride = int(lens.max())
+    K = torch.randn(a.layers, cap, hkv, d, device="cuda").to(torch.bfloat16)
+    V = torch.randn(a.layers, cap, hkv, d, device="cuda").to(torch.bfloat16)
+    perm = rng.permutation(cap)
+    tab = np.zeros((a.batch, stride), np.int32)
+    o = 0
+    for i, n in enumerate(lens):
+        tab[i, :n] = perm[o:o + n]
+        o += n
+    tab_d = torch.from_numpy(tab).cuda()
+    sd = StepDesc()
+    for i, n in enumerate(lens):
+        sd.dec.append((i, i, int(n)))
+    step = torch.from_numpy(sd.pack()).cuda()
+    q = torch.randn(a.batch, hq, d, device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(q)
+    ctas = a.ctas or L.load().tim_sm_count()
+    ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, a.batch, hq, d), device="cuda")
+    cnt = torch.zeros(a.batch, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+
+    def run(l):
+        L.call("tim_attn_decode", step.data_ptr(), q.data_ptr(), out.data_ptr(), K[l].data_ptr(),
+               V[l].data_ptr(), tab_d.data_ptr(), stride, hq, hkv, d, 1 / np.sqrt(d), ws.data_ptr(),
+               cnt.data_ptr(), ctas, a.batch, L.DTYPE_BF16, st)
+
+    for l in range(a.layers):
+        run(l)
+    torch.cuda.synchronize()
+    # back-to-back launches over rotating layers (inputs > L2), so host launch
+    # latency is hidden behind the previous kernel and events time the GPU only
+    times = []
+    for it in range(a.iters):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for l in range(a.layers):
+            run(l)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / a.layers)
+    byts = int(lens.sum()) * hkv * d * 2 * 2 + a.batch * hq * d * 2 * 2
+    ms = float(np.median(times))
+    print(json.dumps({"tokens": int(lens.sum()), "bytes": byts, "ms": ms,
+                      "gbs": byts / ms / 1e6, "ctas": ctas}))
+
+
+if __name__ == "__main__":
+    main()

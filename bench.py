@@ -154,59 +154,96 @@ def run_gpu(args, rank: int, world: int, dist):
             tok += sum(rep.decoded.values())
         return tok
 
+    t0 = time.perf_counter()
+    rt.precapture()
+    print(f"[rank {rank}] captured {len(rt.graphs)} step graphs in {time.perf_counter() - t0:.1f} s",
+          file=sys.stderr)
     steps(args.skip)
     steps(args.warmup)
     barrier()
 
-    # ---- value: device-resident replay of K planned steps -----------------------
-    rt.recording = []
-    planned_tokens = steps(args.steps)
-    records, rt.recording = rt.recording, None
-    resident = rt.replay_upload(records)
-    rt.attn_events = []
-    launches0 = rt.launches
+    # The timed region alternates blocks of `--block` steps: a value block
+    # (steps planned on the host first, then replayed from device-resident
+    # descriptors: GPU-only time) and an e2e block (the next steps through the
+    # public Engine.step(): host planning + pinned H2D of the descriptor + D2H
+    # of the step's greedy tokens).  Both arms thus sample the same phase of
+    # the trajectories; each times exactly `--steps` steps.
+    attn_store = []
+    phase_store = [] if os.environ.get("TIMRUN_PHASES") else None
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
-    clocks.start()
-    barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    rt.replay(resident)
-    e1.record()
-    barrier()
-    clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    launches = rt.launches - launches0
-    attn = [(a.elapsed_time(b), sd) for a, b, sd in rt.attn_events]
-    rt.attn_events = None
-    # dominant-kernel roofline: layer-0 decode attention, algorithmic bytes per launch
-    attn_ms = sum(t for t, _ in attn) / max(len(attn), 1)
-    attn_bytes = sum(sum(d[2] for d in sd.dec) * kv_tok_layer + len(sd.dec) * q_o_bytes
-                     for _, sd in attn) / max(len(attn), 1)
-    mean_live = sum(sum(d[2] for d in sd.dec) / max(len(sd.dec), 1) for _, sd in attn) / max(len(attn), 1)
-
-    # ---- e2e: public Engine.step() with per-step H2D + D2H ----------------------
-    barrier()
-    h2d = d2h = 0
-    w0 = time.perf_counter()
-    f0 = torch.cuda.Event(enable_timing=True)
-    f1 = torch.cuda.Event(enable_timing=True)
-    f0.record()
-    e2e_tokens = 0
     host_buf = torch.empty(args.batch * 2, dtype=torch.int32, pin_memory=True)
-    for _ in range(args.steps):
-        rep = eng.step()
-        e2e_tokens += sum(rep.decoded.values())
-        h2d += rt._last_upload_bytes
-        toks = eng.last_step_tokens
-        if toks is not None:
-            n = toks.numel()
-            host_buf[:n].copy_(toks)           # D2H of the step's result (greedy tokens)
-            d2h += n * 4
-    f1.record()
-    barrier()
-    e2e_ms = f0.elapsed_time(f1)
-    wall_ms = (time.perf_counter() - w0) * 1000.0
+    ms = e2e_ms = wall_ms = 0.0
+    planned_tokens = e2e_tokens = 0
+    launches = h2d = d2h = 0
+    rows = []
+    clocks.start()
+    done = 0
+    while done < args.steps:
+        nb = min(args.block, args.steps - done)
+        rt.recording = []
+        planned_tokens += steps(nb)
+        records, rt.recording = rt.recording, None
+        resident = rt.replay_upload(records)
+        rows += [sd.n_rows for sd, _, _ in records]
+        launches0 = rt.launches
+        rt.attn_events, rt.phase_events = attn_store, phase_store
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rt.replay(resident)
+        e1.record()
+        barrier()
+        ms += e0.elapsed_time(e1)
+        launches += rt.launches - launches0
+        rt.attn_events = rt.phase_events = None
+        w0 = time.perf_counter()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(nb):
+            rep = eng.step()
+            e2e_tokens += sum(rep.decoded.values())
+            h2d += rt._last_upload_bytes
+            toks = eng.last_step_tokens
+            if toks is not None:
+                n = toks.numel()
+                host_buf[:n].copy_(toks)           # D2H of the step's result (greedy tokens)
+                d2h += n * 4
+        f1.record()
+        barrier()
+        e2e_ms += f0.elapsed_time(f1)
+        wall_ms += (time.perf_counter() - w0) * 1000.0
+        done += nb
+    clk = clocks.stop()
+    rows.sort()
+    print(f"[rank {rank}] rows/step in the value blocks: min {rows[0]} median {rows[len(rows) // 2]} "
+          f"p90 {rows[int(len(rows) * 0.9)]} max {rows[-1]} mean {sum(rows) / len(rows):.0f}",
+          file=sys.stderr)
+    if phase_store:
+        import collections
+        agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0, 0])
+        for key, nd, kv, evs in phase_store:
+            a = agg[key]
+            a[0] += 1
+            a[1] += evs[0].elapsed_time(evs[1])
+            a[2] += evs[1].elapsed_time(evs[2])
+            a[3] += evs[2].elapsed_time(evs[3])
+            a[4] += kv
+        for key, (n, p0, p1, p2, kv) in sorted(agg.items()):
+            print(f"[phases] {key}: steps={n} pre={p0/n:.3f}ms attn0={p1/n:.3f}ms post={p2/n:.3f}ms "
+                  f"kv_tokens/step={kv/n:.0f}", file=sys.stderr)
+    # dominant-kernel roofline: the layer-0 attention launch of every value-block step
+    attn = [(a.elapsed_time(b), sd) for a, b, sd in attn_store]
+    attn_ms = sum(t for t, _ in attn) / max(len(attn), 1)
+    # unique K/V of every request's retained pages + its new rows, plus q in / ctx out per row
+    attn_bytes = sum(sum(sg[1] + sg[2] for sg in sd.segs) * kv_tok_layer + sd.n_rows * q_o_bytes
+                     for _, sd in attn) / max(len(attn), 1)
+    dec_only = [(t, sd) for t, sd in attn if sd.n_rows == len(sd.segs)]
+    dec_ms = sum(t for t, _ in dec_only) / max(len(dec_only), 1)
+    dec_bytes = sum(sum(sg[1] + sg[2] for sg in sd.segs) * kv_tok_layer + sd.n_rows * q_o_bytes
+                    for _, sd in dec_only) / max(len(dec_only), 1)
+    mean_live = sum(sum(sg[1] for sg in sd.segs) / max(len(sd.segs), 1) for _, sd in attn) / max(len(attn), 1)
 
     print(f"[rank {rank}] value window: {planned_tokens} tokens in {ms:.1f} ms; e2e window: "
           f"{e2e_tokens} tokens in {e2e_ms:.1f} ms GPU / {wall_ms:.1f} ms wall; "
@@ -215,6 +252,7 @@ def run_gpu(args, rank: int, world: int, dist):
         dist, [ms, e2e_ms], [planned_tokens, e2e_tokens], device="cuda")
     return dict(ms=ms, e2e_ms=e2e_ms, wall_ms=wall_ms, tokens=planned_tokens, e2e_tokens=e2e_tokens,
                 attn_ms=attn_ms, attn_bytes=attn_bytes, launches=launches, clocks=clk,
+                dec_ms=dec_ms, dec_bytes=dec_bytes, n_dec_launches=len(dec_only), n_attn=len(attn),
                 h2d=h2d / args.steps, d2h=d2h / args.steps, mean_live=mean_live,
                 weight_gb=model.weight_bytes() / 1e9)
 
@@ -325,6 +363,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--skip", type=int, default=1500)
+    ap.add_argument("--block", type=int, default=20)
     ap.add_argument("--batch", type=int, default=PER_GPU)
     ap.add_argument("--threshold", type=int, default=2)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -384,7 +423,13 @@ def main():
                          "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                          "peak_src": pk["src"],
-                         "bytes_per_launch": res["attn_bytes"], "ms_per_launch": res["attn_ms"]},
+                         "bytes_per_launch": res["attn_bytes"], "ms_per_launch": res["attn_ms"],
+                         "launches_timed": res["n_attn"],
+                         "decode_only_steps": {"achieved": (res["dec_bytes"] / (res["dec_ms"] * 1e-3) / 1e9)
+                                               if res["dec_ms"] else None,
+                                               "bytes_per_launch": res["dec_bytes"],
+                                               "ms_per_launch": res["dec_ms"],
+                                               "launches": res["n_dec_launches"]}},
             "cpu_baseline": cpu,
             "e2e": {"value": res["e2e_tokens"] / (res["e2e_ms"] * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],

@@ -50,7 +50,7 @@ enum {
  * the same buffer.  Record layouts (int32 fields):
  *   new   : {slot, logical_idx, token, row, live_idx}          host-known tokens
  *   seg   : {slot, m, n, row_off}                               one encode segment
- *   dec   : {row, slot, kv_len}  + dec_prefix[n_dec+1]          split-K decode queries
+ *   dec   : {row, slot, kv_len, nq} + dec_prefix[n_dec+1]       attention query tiles
  *   ext   : {row_off, slot, m, n, q0}                           extend q-tiles
  *   job   : {slot, old_len, suffix_start, reencode_from,
  *            span_off, n_spans, out_row, expect_keep}           prune compaction jobs
@@ -70,7 +70,7 @@ typedef struct {
 
 #define TIM_NEW_FIELDS 5
 #define TIM_SEG_FIELDS 4
-#define TIM_DEC_FIELDS 3
+#define TIM_DEC_FIELDS 4
 #define TIM_EXT_FIELDS 5
 #define TIM_JOB_FIELDS 8
 #define TIM_OP_FIELDS 6
@@ -127,35 +127,52 @@ int32_t tim_rmsnorm(const void* x, int64_t x_stride, void* y, int64_t y_stride, 
 int32_t tim_silu(void* x, int64_t n, int32_t dtype, void* stream);
 
 /* K3: rotate-half RoPE (model.py:118-125) of q and k from the fused qkv GEMM
- * output [rows, (hq + 2 hkv) * D], store roped K and raw V into the page of
- * each row for this layer (model.py:147-148), write roped q to q_out.
- * cos/sin tables are [position_limit, D/2] fp32, built on the host exactly as
- * the reference (fp32 angle pos*inv_freq, model.py:104-105,121). */
-int32_t tim_rope_kv_store(const void* qkv, int32_t n_rows, const int32_t* row_pos,
-                          const int32_t* row_pages, const float* cos_tab, const float* sin_tab,
-                          int32_t hq, int32_t hkv, int32_t head_dim, void* q_out,
-                          void* k_layer, void* v_layer, int32_t dtype, void* stream);
+ * output [rows, (hq + 2 hkv) * D], store roped K and V into the page of each
+ * row for this layer (model.py:147-148), write roped q to q_out.  When `h` is
+ * non-null the row's weightless RMSNorm (model.py:69-70) is applied here as a
+ * per-row scale 1/sqrt(mean(h^2)+eps): the GEMM ran on the raw residual h,
+ * and rms(h) @ W == (h @ W) * scale.  cos/sin tables are [position_limit,
+ * D/2] fp32, built on the host exactly as the reference (fp32 angle
+ * pos*inv_freq, model.py:104-105,121). */
+int32_t tim_rope_kv_store(const void* qkv, const void* h, int32_t dm, float eps, int32_t n_rows,
+                          const int32_t* row_pos, const int32_t* row_pages, const float* cos_tab,
+                          const float* sin_tab, int32_t hq, int32_t hkv, int32_t head_dim,
+                          void* q_out, void* k_layer, void* v_layer, int32_t dtype, void* stream);
+/* u[r,:] = silu(u[r,:] * 1/sqrt(mean(h[r,:]^2)+eps)) in place: the MLP input
+ * RMSNorm folded behind the W1 GEMM (model.py:161). */
+int32_t tim_silu_rms(void* u, int32_t n_rows, int32_t width, const void* h, int32_t dm, float eps,
+                     int32_t dtype, void* stream);
 
-/* K1+K6: split-K (stream-K) paged GQA decode attention over retained pages only
- * (model.py:149-159 with n = 1).  `n_ctas` persistent CTAs split the
- * concatenated kv tokens of all decode queries evenly; queries spanning several
- * CTAs are merged in-kernel by the last CTA (log-sum-exp combine).
- * ws: float workspace of tim_decode_ws_floats(n_ctas, n_dec, hq, D) floats;
- * counters: int32[max_dec] zero-initialised once (self-resetting); max_dec bounds n_dec. */
-int64_t tim_decode_ws_floats(int32_t n_ctas, int32_t max_dec, int32_t hq, int32_t head_dim);
+/* K1+K6: split-K (stream-K) paged GQA attention over retained pages only
+ * (model.py:149-159).  Work items are query tiles {row, slot, kv_len, nq}:
+ * nq consecutive query rows of one request (nq = 1 for decode, up to
+ * tim_extend_queries_per_item for re-encode / prefill / tool rows); query i of
+ * a tile sees keys [0, kv_len - nq + i] (prefix fully visible, causal inside
+ * the new block).  `n_ctas` persistent CTAs split the concatenated key ranges
+ * of all tiles evenly; tiles spanning several CTAs are merged in-kernel by the
+ * last CTA to finish (log-sum-exp combine).
+ * ws: float workspace of tim_decode_ws_floats(n_ctas, max_dec, hkv, D) floats;
+ * counters: int32[max_dec * hkv] zero-initialised once (self-resetting); max_dec bounds n_dec. */
+int64_t tim_decode_ws_floats(int32_t n_ctas, int32_t max_dec, int32_t hkv, int32_t head_dim);
 int32_t tim_attn_decode(const int32_t* step, const void* q, void* out, const void* k_layer,
                         const void* v_layer, const int32_t* block_tables, int64_t table_stride,
                         int32_t hq, int32_t hkv, int32_t head_dim, float scale, float* ws,
                         int32_t* counters, int32_t n_ctas, int32_t max_dec, int32_t dtype,
                         void* stream);
 
-/* K2: extend / re-encode attention: q-tiles of a multi-token segment attend the
- * paged prefix table[slot][0..m) plus the causal new block (model.py:139-140,155). */
+/* Diagnostics: per-CTA %globaltimer timeline of tim_attn_decode written to
+ * buf[4*cta .. 4*cta+3] = {start, first stage landed, main loop end, end};
+ * pass NULL to disable. */
+int32_t tim_set_trace(void* buf);
+
+/* Reference-precision attention (fp32, or shapes outside the tensor-core
+ * kernel): every row of the step's segments attends its paged prefix plus the
+ * causal new block (model.py:139-140,149-159); max_items bounds the rows. */
 int32_t tim_attn_extend(const int32_t* step, int32_t max_items, const void* q, void* out,
                         const void* k_layer, const void* v_layer, const int32_t* block_tables,
                         int64_t table_stride, int32_t hq, int32_t hkv, int32_t head_dim,
                         float scale, int32_t dtype, void* stream);
-/* Queries per extend item for a given config (the host tiles segments with it). */
+/* Queries per attention tile of tim_attn_decode for a config (the host tiles segments with it). */
 int32_t tim_extend_queries_per_item(int32_t hq, int32_t hkv, int32_t head_dim, int32_t dtype);
 
 /* Greedy argmax over rows of logits [n, vocab] (lowest id on ties, model.py:186-192). */

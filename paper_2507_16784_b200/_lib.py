@@ -28,7 +28,7 @@ OP_ALLOC = 0
 OP_FREE = 1
 
 HEADER_INTS = 32
-NEW_FIELDS, SEG_FIELDS, DEC_FIELDS, EXT_FIELDS, JOB_FIELDS, OP_FIELDS = 5, 4, 3, 5, 8, 6
+NEW_FIELDS, SEG_FIELDS, DEC_FIELDS, EXT_FIELDS, JOB_FIELDS, OP_FIELDS = 5, 4, 4, 5, 8, 6
 
 # Every exported symbol with its ctypes signature (checked by tests/test_abi.py).
 _i32, _i64, _f32, _p, _cp = C.c_int32, C.c_int64, C.c_float, C.c_void_p, C.c_char_p
@@ -44,13 +44,16 @@ SIGNATURES = {
     "tim_embed": (_i32, [_p, _i32, _p, _i32, _p, _i32, _p]),
     "tim_rmsnorm": (_i32, [_p, _i64, _p, _i64, _i32, _i32, _f32, _i32, _p]),
     "tim_silu": (_i32, [_p, _i64, _i32, _p]),
-    "tim_rope_kv_store": (_i32, [_p, _i32, _p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _i32, _p]),
+    "tim_rope_kv_store": (_i32, [_p, _p, _i32, _f32, _i32, _p, _p, _p, _p, _i32, _i32, _i32, _p, _p,
+                                 _p, _i32, _p]),
+    "tim_silu_rms": (_i32, [_p, _i32, _i32, _p, _i32, _f32, _i32, _p]),
     "tim_decode_ws_floats": (_i64, [_i32, _i32, _i32, _i32]),
     "tim_attn_decode": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _i32, _f32, _p, _p, _i32,
                                _i32, _i32, _p]),
     "tim_attn_extend": (_i32, [_p, _i32, _p, _p, _p, _p, _p, _i64, _i32, _i32, _i32, _f32, _i32, _p]),
     "tim_extend_queries_per_item": (_i32, [_i32, _i32, _i32, _i32]),
     "tim_argmax": (_i32, [_p, _i32, _i32, _p, _i32, _p]),
+    "tim_set_trace": (_i32, [_p]),
 }
 
 

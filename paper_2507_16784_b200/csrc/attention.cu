@@ -16,8 +16,9 @@
 //   cores (mma.sync m16n8k16 bf16, fp32 accumulate) with an online softmax.
 //   Queries split across CTAs are merged in-kernel (K6) by the last CTA to
 //   finish (threadfence + counter), with a log-sum-exp combine.
-// K2 (extend / re-encode, bf16 KV): FA2-style q-tiles of 64 rows
-//   (queries x group heads) per (item, kv head), cp.async 3-stage ring.
+//   The same kernel serves extend / re-encode / prefill rows: a work item is
+//   a tile of up to 16/group consecutive queries (rows = queries x group
+//   heads of the MMA tile) with a causal limit per query.
 // Generic (fp32 / any): warp per (row, q head), exact two-pass softmax; used
 //   for the fp32 parity configuration.
 #include "common.cuh"
@@ -25,9 +26,9 @@
 namespace tim {
 
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kMaxHeads = 128;      // hq bound for the in-kernel combine
-constexpr int kCombineChunk = 8;    // partials merged per smem pass
 constexpr int kIdChunk = 1024;      // page ids staged per producer refill (multiple of TK)
+constexpr int kFastPieces = 4;      // partials merged by the one-round-trip combine
+constexpr int kMinTokensPerCta = 64;  // below this many kv tokens per CTA, use fewer CTAs
 
 // ===================================================================== K1
 template <int D, int HKV>
@@ -43,6 +44,16 @@ struct DecCfg {
   static constexpr int KC = D / 16;
   static constexpr int NT = D / 8;
 };
+
+// Optional per-CTA timeline (%globaltimer, ns): [start, first data, loop end,
+// end] for CTA c at g_trace[4c..4c+3]; enabled by tim_set_trace (diagnostics).
+__device__ unsigned long long* g_trace = nullptr;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ int64_t cta_of(int64_t x, int64_t G, int64_t N) {
   return ((x + 1) * G - 1) / N;
@@ -60,14 +71,15 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
   int* sflag = reinterpret_cast<int*>(empty + C::STAGES);
-  __shared__ float s_m[kMaxHeads], s_inv[kMaxHeads];
-  __shared__ float s_w[kCombineChunk][kMaxHeads];
 
+  unsigned long long* trace = g_trace;
+  if (trace && threadIdx.x == 0) trace[4 * blockIdx.x] = gtimer();
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
   const int n_dec = hd.n_dec;
   const int64_t N = hd.dec_total;
   if (n_dec == 0 || N == 0) return;
-  const int64_t G = gridDim.x < N ? gridDim.x : N;
+  const int64_t want = (N + kMinTokensPerCta - 1) / kMinTokensPerCta;
+  const int64_t G = gridDim.x < want ? gridDim.x : want;
   const int c = blockIdx.x;
   if (c >= G) return;
   const int32_t* dec = step + hd.off_dec;
@@ -113,6 +125,10 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
 #pragma unroll 8
         for (int i = lane; i < c1 - c0; i += 32) s_ids[i] = __ldg(trow + c0 + i);
         __syncwarp();
+        // Programmatic dependent launch: block tables were written by earlier
+        // kernels; the K/V rows of this step's tokens and q come from the
+        // kernel right before us (RoPE+store), so wait for it only now.
+        if (it == 0) griddep_wait();
         for (int k0 = c0; k0 < c1; k0 += C::TK, ++it) {
           const int ntok = (c1 - k0) < C::TK ? (c1 - k0) : C::TK;
           const int stg = it % C::STAGES;
@@ -131,33 +147,49 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
   }
 
   // -------------------------------------------------------------- consumers
-  const int grp = hq / HKV;             // q heads per kv head (rows used of the m16 tile)
+  griddep_wait();
+  // A work item is a query tile: nq consecutive queries of one request (1 for
+  // decode, up to 16/grp for extend / re-encode rows) x the grp q heads of
+  // this warp's kv head = the 16 rows of the m16n8k16 tile (row rr = query
+  // rr/grp, head rr%grp).  Query qi of the tile sees keys <= kv_len-nq+qi
+  // (prefix fully visible, causal inside the new block, model.py:139-140).
+  const int grp = hq / HKV;
   const int g = lane >> 2, t = lane & 3;
   const float sl = scale * kLog2e;
   const uint32_t smem_base = smem_u32(smem);
+  const int64_t slot_floats = (int64_t)HKV * 16 * D;   // one partial: 16 rows per kv head
   float* ws_o = ws;
-  float* ws_ml = ws + (int64_t)(gridDim.x + max_dec) * hq * D;
+  float* ws_ml = ws + (int64_t)(gridDim.x + max_dec) * slot_floats;
   int it = 0;
 
   for (int r = r0; r < n_dec && prefix[r] < end; ++r) {
     const int64_t lo = prefix[r], hi = prefix[r + 1];
     const int p0 = (int)((start > lo ? start : lo) - lo);
     const int p1 = (int)((end < hi ? end : hi) - lo);
-    const int qrow = dec[r * TIM_DEC_FIELDS + 0];
+    const int32_t* rec = dec + r * TIM_DEC_FIELDS;
+    const int qrow = rec[0], kv_len = rec[2], nq = rec[3];
+    const int nrows = nq * grp;
 
-    // Q fragments (A operand, rows = heads of this kv group, k = d)
+    int lim[2], orow[2];
+    bool valid[2];
     uint32_t qa[C::KC][4];
-    {
-      const __nv_bfloat16* qb = q + ((int64_t)qrow * hq + warp * grp) * D;
 #pragma unroll
-      for (int kc = 0; kc < C::KC; ++kc) {
-        const int d0 = kc * 16 + 2 * t;
-        qa[kc][0] = g < grp ? *reinterpret_cast<const uint32_t*>(qb + g * D + d0) : 0u;
-        qa[kc][1] = g + 8 < grp ? *reinterpret_cast<const uint32_t*>(qb + (g + 8) * D + d0) : 0u;
-        qa[kc][2] = g < grp ? *reinterpret_cast<const uint32_t*>(qb + g * D + d0 + 8) : 0u;
-        qa[kc][3] = g + 8 < grp ? *reinterpret_cast<const uint32_t*>(qb + (g + 8) * D + d0 + 8) : 0u;
-      }
+    for (int h = 0; h < 2; ++h) {
+      const int rr = g + 8 * h;
+      valid[h] = rr < nrows;
+      const int qi = rr / grp;
+      lim[h] = kv_len - nq + qi;                          // last visible key (absolute)
+      orow[h] = (qrow + qi) * hq + warp * grp + (rr - qi * grp);
     }
+#pragma unroll
+    for (int kc = 0; kc < C::KC; ++kc) {
+      const int d0 = kc * 16 + 2 * t;
+      qa[kc][0] = valid[0] ? *reinterpret_cast<const uint32_t*>(q + (int64_t)orow[0] * D + d0) : 0u;
+      qa[kc][1] = valid[1] ? *reinterpret_cast<const uint32_t*>(q + (int64_t)orow[1] * D + d0) : 0u;
+      qa[kc][2] = valid[0] ? *reinterpret_cast<const uint32_t*>(q + (int64_t)orow[0] * D + d0 + 8) : 0u;
+      qa[kc][3] = valid[1] ? *reinterpret_cast<const uint32_t*>(q + (int64_t)orow[1] * D + d0 + 8) : 0u;
+    }
+
     float o[C::NT][4];
 #pragma unroll
     for (int i = 0; i < C::NT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
@@ -167,6 +199,7 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
       const int ntok = (p1 - k0) < C::TK ? (p1 - k0) : C::TK;
       const int stg = it % C::STAGES;
       mbar_wait(&full[stg], (it / C::STAGES) & 1);
+      if (trace && it == 0 && threadIdx.x == 0) trace[4 * blockIdx.x + 1] = gtimer();
       const uint32_t kbase = smem_base + stg * C::STAGE_BYTES + warp * D * 2;
       const uint32_t vbase = kbase + C::TK * C::ROW_STRIDE;
 
@@ -192,7 +225,7 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
         float mx = -INFINITY;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          v[h][j] = tk[j] < ntok ? v[h][j] * sl : -INFINITY;
+          v[h][j] = (tk[j] < ntok && k0 + tk[j] <= lim[h]) ? v[h][j] * sl : -INFINITY;
           mx = fmaxf(mx, v[h][j]);
         }
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
@@ -236,7 +269,12 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
       if (lane == 0) mbar_arrive(&empty[stg]);
     }
 
+    if (trace && threadIdx.x == 0) trace[4 * blockIdx.x + 2] = gtimer();
     // ------------------------------------------------------------ epilogue
+    // Per warp (= per kv-head group), no CTA barrier: a tile covered by one
+    // CTA is written directly; otherwise the warp stores its unnormalised
+    // partial (O, m, l per row) and bumps the (tile, kv head) counter with an
+    // acq_rel atomic; the warp that arrives last merges the partials (K6).
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 1);
@@ -247,10 +285,9 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
     if (npieces == 1) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int rr = g + 8 * h;
-        if (rr < grp) {
+        if (valid[h]) {
           const float inv = 1.f / l_r[h];
-          __nv_bfloat16* ob = out + ((int64_t)qrow * hq + warp * grp + rr) * D;
+          __nv_bfloat16* ob = out + (int64_t)orow[h] * D;
 #pragma unroll
           for (int i = 0; i < C::NT; ++i)
             *reinterpret_cast<uint32_t*>(ob + i * 8 + 2 * t) =
@@ -259,269 +296,92 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
       }
       continue;
     }
-    const int64_t slot = c + r;
+    const int64_t wslot = ((c + r) * HKV + warp) * 16;   // first of this warp's 16 partial rows
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int rr = g + 8 * h;
-      if (rr < grp) {
-        const int head = warp * grp + rr;
-        float* ob = ws_o + (slot * hq + head) * D;
+      if (valid[h]) {
+        float* ob = ws_o + (wslot + rr) * D;
 #pragma unroll
         for (int i = 0; i < C::NT; ++i)
           __stcg(reinterpret_cast<float2*>(ob + i * 8 + 2 * t), make_float2(o[i][2 * h], o[i][2 * h + 1]));
-        if (t == 0) __stcg(reinterpret_cast<float2*>(ws_ml + (slot * hq + head) * 2), make_float2(m_r[h], l_r[h]));
+        if (t == 0) __stcg(reinterpret_cast<float2*>(ws_ml + (wslot + rr) * 2), make_float2(m_r[h], l_r[h]));
       }
     }
-    __threadfence();
-    asm volatile("bar.sync 1, %0;" ::"n"(HKV * 32));
-    if (threadIdx.x == 0) {
-      const int old = atomicAdd(&counters[r], 1);
-      const int last = old == npieces - 1;
-      if (last) counters[r] = 0;
-      *sflag = last;
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      int old;
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                   : "=r"(old) : "l"(counters + (int64_t)r * HKV + warp) : "memory");
+      last = old == npieces - 1;
+      if (last) counters[(int64_t)r * HKV + warp] = 0;
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(HKV * 32));
-    if (*sflag) {
-      __threadfence();
-      // K6: log-sum-exp merge of this query's partials (slots c' + r).  Per
-      // head: M = max m_p, weight_p = exp2(m_p - M) / sum_q exp2(m_q - M) l_q;
-      // then every thread merges float4 slices of the hq*D outputs.
-      const int nthr = HKV * 32;
-      for (int h = threadIdx.x; h < hq; h += nthr) {
-        float M = -INFINITY;
-        for (int64_t cc = c_first; cc <= c_last; ++cc)
-          M = fmaxf(M, __ldcg(ws_ml + ((cc + r) * hq + h) * 2));
-        float den = 0.f;
-        for (int64_t cc = c_first; cc <= c_last; ++cc) {
-          const float2 ml = __ldcg(reinterpret_cast<const float2*>(ws_ml + ((cc + r) * hq + h) * 2));
-          den += (ml.x == -INFINITY ? 0.f : fast_exp2(ml.x - M)) * ml.y;
-        }
-        s_m[h] = M;
-        s_inv[h] = 1.f / den;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) continue;
+    // K6 for this warp's rows: out = sum_p exp2(m_p - M) O_p / sum_p exp2(m_p - M) l_p.
+    // Rows are merged 4 at a time and partials kFastPieces at a time with an
+    // online (running-max) merge; every load of a chunk is issued before any
+    // use, so a decode tile over <= kFastPieces partials costs one round trip.
+    for (int r0w = 0; r0w < nrows; r0w += 4) {
+      float M[4], den[4];
+      float4 acc[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        M[k] = -INFINITY;
+        den[k] = 0.f;
+        acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      constexpr int V4 = 4;  // float4 slices per thread per pass
-      const int n4 = hq * D / 4;
-      for (int base = 0; base < n4; base += nthr * V4) {
-        float4 acc[V4];
+      for (int64_t cb = c_first; cb <= c_last; cb += kFastPieces) {
+        float2 ml[4][kFastPieces];
+        float4 ov[4][kFastPieces];
 #pragma unroll
-        for (int k = 0; k < V4; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int64_t c0 = c_first; c0 <= c_last; c0 += kCombineChunk) {
-          const int np = (int)((c_last - c0 + 1) < kCombineChunk ? (c_last - c0 + 1) : kCombineChunk);
-          asm volatile("bar.sync 1, %0;" ::"n"(HKV * 32));
-          for (int i = threadIdx.x; i < np * hq; i += nthr) {
-            const int pp = i / hq, h = i - pp * hq;
-            const float mm = __ldcg(ws_ml + ((c0 + pp + r) * hq + h) * 2);
-            s_w[pp][h] = mm == -INFINITY ? 0.f : fast_exp2(mm - s_m[h]) * s_inv[h];
-          }
-          asm volatile("bar.sync 1, %0;" ::"n"(HKV * 32));
-          for (int pp = 0; pp < np; ++pp) {
-            const float4* src = reinterpret_cast<const float4*>(ws_o + (c0 + pp + r) * hq * D);
+        for (int k = 0; k < 4; ++k) {
 #pragma unroll
-            for (int k = 0; k < V4; ++k) {
-              const int e4 = base + threadIdx.x + k * nthr;
-              if (e4 < n4) {
-                const float w = s_w[pp][(e4 * 4) / D];
-                const float4 v = __ldcg(src + e4);
-                acc[k].x += w * v.x; acc[k].y += w * v.y; acc[k].z += w * v.z; acc[k].w += w * v.w;
-              }
+          for (int p = 0; p < kFastPieces; ++p) {
+            ml[k][p] = make_float2(-INFINITY, 0.f);
+            ov[k][p] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (r0w + k < nrows && cb + p <= c_last) {
+              const int64_t pr = ((cb + p + r) * HKV + warp) * 16 + r0w + k;
+              ml[k][p] = __ldcg(reinterpret_cast<const float2*>(ws_ml + pr * 2));
+              if (lane * 4 < D) ov[k][p] = __ldcg(reinterpret_cast<const float4*>(ws_o + pr * D) + lane);
             }
           }
         }
 #pragma unroll
-        for (int k = 0; k < V4; ++k) {
-          const int e4 = base + threadIdx.x + k * nthr;
-          if (e4 < n4) {
-            uint2 pk;
-            pk.x = pack_bf16(acc[k].x, acc[k].y);
-            pk.y = pack_bf16(acc[k].z, acc[k].w);
-            *reinterpret_cast<uint2*>(out + (int64_t)qrow * hq * D + e4 * 4) = pk;
+        for (int k = 0; k < 4; ++k) {
+          float mc = M[k];
+#pragma unroll
+          for (int p = 0; p < kFastPieces; ++p) mc = fmaxf(mc, ml[k][p].x);
+          const float sc = M[k] == -INFINITY ? 0.f : fast_exp2(M[k] - mc);
+          den[k] *= sc;
+          acc[k].x *= sc; acc[k].y *= sc; acc[k].z *= sc; acc[k].w *= sc;
+#pragma unroll
+          for (int p = 0; p < kFastPieces; ++p) {
+            const float w = ml[k][p].x == -INFINITY ? 0.f : fast_exp2(ml[k][p].x - mc);
+            den[k] += w * ml[k][p].y;
+            acc[k].x += w * ov[k][p].x; acc[k].y += w * ov[k][p].y;
+            acc[k].z += w * ov[k][p].z; acc[k].w += w * ov[k][p].w;
           }
+          M[k] = mc;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int rr = r0w + k;
+        if (rr < nrows && lane * 4 < D) {
+          const int qi = rr / grp;
+          const int64_t oidx = (int64_t)(qrow + qi) * hq + warp * grp + (rr - qi * grp);
+          const float inv = 1.f / den[k];
+          uint2 pk;
+          pk.x = pack_bf16(acc[k].x * inv, acc[k].y * inv);
+          pk.y = pack_bf16(acc[k].z * inv, acc[k].w * inv);
+          *reinterpret_cast<uint2*>(out + oidx * D + lane * 4) = pk;
         }
       }
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(HKV * 32));
   }
-}
-
-// ===================================================================== K2
-template <int D>
-struct ExtCfg {
-  static constexpr int TK = 32;
-  static constexpr int ROW_BYTES = D * 2;
-  static constexpr int ROW_STRIDE = ROW_BYTES + 16;
-  static constexpr int STAGES = 3;
-  static constexpr int STAGE_BYTES = 2 * TK * ROW_STRIDE;
-  static constexpr int THREADS = 128;  // 4 warps x 16 rows
-  static constexpr int SMEM = STAGES * STAGE_BYTES;
-  static constexpr int KC = D / 16;
-  static constexpr int NT = D / 8;
-  static constexpr int CHUNKS = ROW_BYTES / 16;
-};
-
-template <int D>
-__global__ void __launch_bounds__(ExtCfg<D>::THREADS)
-    attn_extend_kernel(const int32_t* __restrict__ step, const __nv_bfloat16* __restrict__ q,
-                       __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kl,
-                       const __nv_bfloat16* __restrict__ vl, const int32_t* __restrict__ tables,
-                       int64_t tstride, int hq, int hkv, float scale) {
-  using C = ExtCfg<D>;
-  extern __shared__ __align__(128) uint8_t smem[];
-  const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
-  if ((int)blockIdx.x >= hd.n_ext) return;
-  const int32_t* item = step + hd.off_ext + blockIdx.x * TIM_EXT_FIELDS;
-  const int row_off = item[0], slot = item[1], m = item[2], n = item[3], q0 = item[4];
-  const int kvh = blockIdx.y;
-  const int grp = hq / hkv;
-  const int qpw = 16 / grp;                   // queries per warp
-  const int q_end = (q0 + 4 * qpw) < n ? (q0 + 4 * qpw) : n;
-  const int kend = m + q_end;                 // keys [0, kend)
-  const int32_t* trow = tables + (int64_t)slot * tstride;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const float sl = scale * kLog2e;
-
-  // rows of this warp: rr -> (query qi, head)
-  int qi_r[2], valid_r[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int rr = g + 8 * h;
-    qi_r[h] = q0 + warp * qpw + rr / grp;
-    valid_r[h] = qi_r[h] < n;
-  }
-  uint32_t qa[C::KC][4];
-#pragma unroll
-  for (int kc = 0; kc < C::KC; ++kc) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int rr = g + 8 * h;
-      const __nv_bfloat16* qb = q + ((int64_t)(row_off + qi_r[h]) * hq + kvh * grp + rr % grp) * D + kc * 16 + 2 * t;
-      qa[kc][h] = valid_r[h] ? *reinterpret_cast<const uint32_t*>(qb) : 0u;
-      qa[kc][h + 2] = valid_r[h] ? *reinterpret_cast<const uint32_t*>(qb + 8) : 0u;
-    }
-  }
-
-  auto load_tile = [&](int tile, int stg) {
-    const int k0 = tile * C::TK;
-    uint8_t* kb = smem + stg * C::STAGE_BYTES;
-    uint8_t* vb = kb + C::TK * C::ROW_STRIDE;
-    for (int e = threadIdx.x; e < C::TK * C::CHUNKS; e += C::THREADS) {
-      const int row = e / C::CHUNKS, ch = e - row * C::CHUNKS;
-      int tok = k0 + row;
-      tok = tok < kend ? tok : kend - 1;
-      const int64_t page = trow[tok];
-      const int64_t off = (page * hkv + kvh) * D + ch * 8;
-      cp_async16(kb + row * C::ROW_STRIDE + ch * 16, kl + off);
-      cp_async16(vb + row * C::ROW_STRIDE + ch * 16, vl + off);
-    }
-  };
-
-  float o[C::NT][4];
-#pragma unroll
-  for (int i = 0; i < C::NT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
-  const int ntiles = (kend + C::TK - 1) / C::TK;
-#pragma unroll
-  for (int s = 0; s < C::STAGES - 1; ++s) {
-    if (s < ntiles) load_tile(s, s);
-    cp_async_commit();
-  }
-  const uint32_t smem_base = smem_u32(smem);
-  for (int tile = 0; tile < ntiles; ++tile) {
-    const int nxt = tile + C::STAGES - 1;
-    if (nxt < ntiles) load_tile(nxt, nxt % C::STAGES);
-    cp_async_commit();
-    cp_async_wait<C::STAGES - 1>();
-    __syncthreads();
-    const int stg = tile % C::STAGES;
-    const uint32_t kbase = smem_base + stg * C::STAGE_BYTES;
-    const uint32_t vbase = kbase + C::TK * C::ROW_STRIDE;
-    const int k0 = tile * C::TK;
-
-    float s[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
-#pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {  // token blocks of 16
-      const int mi = lane >> 3;
-      const int tok = nb * 16 + (lane & 7) + (mi >> 1) * 8;
-      const uint32_t a = kbase + tok * C::ROW_STRIDE + (mi & 1) * 16;
-#pragma unroll
-      for (int kc = 0; kc < C::KC; ++kc) {
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(b0, b1, b2, b3, a + kc * 32);
-        mma_bf16(s[2 * nb], qa[kc][0], qa[kc][1], qa[kc][2], qa[kc][3], b0, b1);
-        mma_bf16(s[2 * nb + 1], qa[kc][0], qa[kc][1], qa[kc][2], qa[kc][3], b2, b3);
-      }
-    }
-    float corr[2];
-    float p[2][8];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int lim = m + qi_r[h];  // causal: key j visible iff j <= m + qi
-      float mx = -INFINITY;
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int key = k0 + nt * 8 + 2 * t + j;
-          const float x = (key <= lim && key < kend) ? s[nt][2 * h + j] * sl : -INFINITY;
-          p[h][nt * 2 + j] = x;
-          mx = fmaxf(mx, x);
-        }
-      }
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      const float mnew = fmaxf(m_r[h], mx);
-      const float muse = mnew == -INFINITY ? 0.f : mnew;
-      corr[h] = fast_exp2(m_r[h] - muse);
-      float sum = 0.f;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        p[h][j] = fast_exp2(p[h][j] - muse);
-        sum += p[h][j];
-      }
-      l_r[h] = l_r[h] * corr[h] + sum;
-      m_r[h] = mnew;
-    }
-#pragma unroll
-    for (int i = 0; i < C::NT; ++i) {
-      o[i][0] *= corr[0];
-      o[i][1] *= corr[0];
-      o[i][2] *= corr[1];
-      o[i][3] *= corr[1];
-    }
-#pragma unroll
-    for (int kb = 0; kb < 2; ++kb) {  // k16 blocks of tokens
-      const uint32_t pa0 = pack_bf16(p[0][kb * 4 + 0], p[0][kb * 4 + 1]);
-      const uint32_t pa1 = pack_bf16(p[1][kb * 4 + 0], p[1][kb * 4 + 1]);
-      const uint32_t pa2 = pack_bf16(p[0][kb * 4 + 2], p[0][kb * 4 + 3]);
-      const uint32_t pa3 = pack_bf16(p[1][kb * 4 + 2], p[1][kb * 4 + 3]);
-      const int mi = lane >> 3;
-      const int tok = kb * 16 + (lane & 7) + (mi & 1) * 8;
-      const uint32_t a = vbase + tok * C::ROW_STRIDE + (mi >> 1) * 16;
-#pragma unroll
-      for (int j = 0; j < C::NT / 2; ++j) {
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(b0, b1, b2, b3, a + j * 32);
-        mma_bf16(o[2 * j], pa0, pa1, pa2, pa3, b0, b1);
-        mma_bf16(o[2 * j + 1], pa0, pa1, pa2, pa3, b2, b3);
-      }
-    }
-    __syncthreads();
-  }
-  cp_async_wait<0>();
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 1);
-    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 2);
-    if (!valid_r[h]) continue;
-    const int rr = g + 8 * h;
-    const float inv = 1.f / l_r[h];
-    __nv_bfloat16* ob = out + ((int64_t)(row_off + qi_r[h]) * hq + kvh * grp + rr % grp) * D;
-#pragma unroll
-    for (int i = 0; i < C::NT; ++i)
-      *reinterpret_cast<uint32_t*>(ob + i * 8 + 2 * t) = pack_bf16(o[i][2 * h] * inv, o[i][2 * h + 1] * inv);
-  }
+  if (trace && threadIdx.x == 0) trace[4 * blockIdx.x + 3] = gtimer();
 }
 
 // ================================================================ generic
@@ -603,27 +463,25 @@ int32_t launch_decode(const int32_t* step, const void* q, void* out, const void*
     cudaFuncSetAttribute(attn_decode_kernel<D, HKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
-  attn_decode_kernel<D, HKV><<<n_ctas, C::THREADS, C::SMEM, st>>>(
-      step, (const __nv_bfloat16*)q, (__nv_bfloat16*)out, (const __nv_bfloat16*)kl,
-      (const __nv_bfloat16*)vl, tables, tstride, hq, scale, ws, counters, max_dec);
-  return check_launch("attn_decode");
-}
-
-template <int D>
-int32_t launch_extend(const int32_t* step, int max_items, const void* q, void* out, const void* kl,
-                      const void* vl, const int32_t* tables, int64_t tstride, int hq, int hkv,
-                      float scale, cudaStream_t st) {
-  using C = ExtCfg<D>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_extend_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_ctas);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(
+      &cfg, attn_decode_kernel<D, HKV>, step, (const __nv_bfloat16*)q, (__nv_bfloat16*)out,
+      (const __nv_bfloat16*)kl, (const __nv_bfloat16*)vl, tables, tstride, hq, scale, ws, counters,
+      max_dec);
+  if (e != cudaSuccess) {
+    set_last_error("attn_decode launch: %s", cudaGetErrorString(e));
+    return TIM_CUDA_ERROR;
   }
-  dim3 grid(max_items, hkv);
-  attn_extend_kernel<D><<<grid, C::THREADS, C::SMEM, st>>>(
-      step, (const __nv_bfloat16*)q, (__nv_bfloat16*)out, (const __nv_bfloat16*)kl,
-      (const __nv_bfloat16*)vl, tables, tstride, hq, hkv, scale);
-  return check_launch("attn_extend");
+  return check_launch("attn_decode");
 }
 
 }  // namespace tim
@@ -638,12 +496,13 @@ static bool tensor_core_shape(int32_t hq, int32_t hkv, int32_t head_dim) {
   return grp_ok && hkv_ok && (head_dim == 64 || head_dim == 128);
 }
 
-extern "C" int64_t tim_decode_ws_floats(int32_t n_ctas, int32_t max_dec, int32_t hq, int32_t head_dim) {
-  return (int64_t)(n_ctas + max_dec) * hq * (head_dim + 2);
+extern "C" int64_t tim_decode_ws_floats(int32_t n_ctas, int32_t max_dec, int32_t hkv, int32_t head_dim) {
+  return (int64_t)(n_ctas + max_dec) * hkv * 16 * (head_dim + 2);
 }
 
 extern "C" int32_t tim_extend_queries_per_item(int32_t hq, int32_t hkv, int32_t head_dim, int32_t dtype) {
-  if (dtype == TIM_DTYPE_BF16 && tensor_core_shape(hq, hkv, head_dim)) return 64 / (hq / hkv);
+  // queries per attention work tile of tim_attn_decode (16 MMA rows / group)
+  if (dtype == TIM_DTYPE_BF16 && tensor_core_shape(hq, hkv, head_dim)) return 16 / (hq / hkv);
   return 1 << 30;  // generic path: whole segments
 }
 
@@ -696,14 +555,19 @@ extern "C" int32_t tim_attn_extend(const int32_t* step, int32_t max_items, const
                                    const int32_t* block_tables, int64_t table_stride, int32_t hq,
                                    int32_t hkv, int32_t head_dim, float scale, int32_t dtype,
                                    void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+  // Reference-precision path (fp32, or shapes outside the tensor-core
+  // kernel): every row of the step's segments; max_items bounds the rows.
   if (max_items <= 0) return TIM_OK;
-  if (dtype == TIM_DTYPE_BF16 && tensor_core_shape(hq, hkv, head_dim)) {
-    if (head_dim == 128)
-      return launch_extend<128>(step, max_items, q, out, k_layer, v_layer, block_tables, table_stride, hq, hkv, scale, st);
-    return launch_extend<64>(step, max_items, q, out, k_layer, v_layer, block_tables, table_stride, hq, hkv, scale, st);
-  }
-  // generic path: max_items is the number of rows to cover
   return launch_generic(step, max_items, q, out, k_layer, v_layer, block_tables, table_stride, hq,
-                        hkv, head_dim, scale, dtype, st);
+                        hkv, head_dim, scale, dtype, (cudaStream_t)stream);
+}
+
+extern "C" int32_t tim_set_trace(void* buf) {
+  unsigned long long* p = (unsigned long long*)buf;
+  const cudaError_t e = cudaMemcpyToSymbol(tim::g_trace, &p, sizeof(p));
+  if (e != cudaSuccess) {
+    tim::set_last_error("set_trace: %s", cudaGetErrorString(e));
+    return TIM_CUDA_ERROR;
+  }
+  return TIM_OK;
 }

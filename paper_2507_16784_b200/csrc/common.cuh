@@ -98,6 +98,12 @@ TIM_DEV uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Programmatic dependent launch (sm_90+): a dependent grid may start early;
+// griddep_wait() blocks until the preceding grid finished and its memory is
+// visible, griddep_launch() lets the next grid start.
+TIM_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+TIM_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 TIM_DEV float fast_exp2(float x) {
   float y;
   asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -168,6 +168,7 @@ class StepRuntime:
         self.graph_pool = None
         self.gstep = None
         self.recording = None        # list -> record descriptors instead of executing
+        self.phase_events = None     # list -> CUDA events around pre / attn0 / post (diagnostics)
         self.attn_events = None      # list -> CUDA events around layer-0 decode attention
 
     # ----------------------------------------------------------- buffers
@@ -212,7 +213,12 @@ class StepRuntime:
         return self.step_dev[:n]
 
     # -------------------------------------------------------------- step
-    GRAPH_BUCKETS = (64, 128, 256, 512, 1024)
+    # Row buckets of the captured forward graphs.  Fine-grained because steps
+    # with re-encode / tool rows are GEMM-compute heavy (~10 GFLOP per row over
+    # 36 layers at the C2 shape): padding 300 rows to 512 would cost ~40 %.
+    # Larger steps run eagerly at their exact row count.
+    GRAPH_BUCKETS = (64, 96, 128, 160, 192, 224, 256, 320, 384, 448, 512, 640, 768, 896, 1024,
+                     1280, 1536, 1792, 2048, 2560, 3072, 3584, 4096)
 
     def graph_bucket(self, n_rows: int):
         if not self.use_graphs:
@@ -221,6 +227,29 @@ class StepRuntime:
             if n_rows <= b:
                 return b
         return None
+
+    def precapture(self) -> None:
+        """Capture every (row bucket, has-extend) forward graph up front, on a
+        sanitised empty step (no rows: page -1 everywhere, no decode/extend
+        work), so no capture ever lands inside a timed region."""
+        if not self.use_graphs:
+            return
+        self._ensure_rows(self.GRAPH_BUCKETS[-1])
+        for b in self.GRAPH_BUCKETS:
+            sd = StepDesc()
+            sd.rows_pad = b
+            sd.last_pad = self.max_slots
+            arr = sd.pack()
+            if self.gstep is None or self.gstep.numel() < arr.size:
+                self.gstep = torch.zeros(1 << 16, dtype=torch.int32, device=self.dev)
+            self.gstep[: arr.size].copy_(torch.from_numpy(arr))
+            L.call("tim_stage_rows", self.gstep.data_ptr(), self.tables.data_ptr(),
+                   self.tables.shape[1], self.live.data_ptr(), self.live.shape[1],
+                   self.logical.data_ptr(), self.logical.shape[1], self.row_tokens.data_ptr(),
+                   self.row_pages.data_ptr(), self.row_pos.data_ptr(), stream_handle())
+            if b not in self.graphs:
+                self.graphs[b] = self.model._capture(self, b, self.max_slots)
+        torch.cuda.synchronize()
 
     def run_step(self, sd: StepDesc, forward: bool = True):
         """Execute one planned step; returns the greedy tokens of sd.last rows
@@ -404,11 +433,11 @@ class B200Transformer:
         """Attention work records for one segment: split-K decode for single-row
         tensor-core segments, q-tiles for the rest."""
         sd.segs.append((slot, m, n, row_off))
-        if self.tensor_cores and n == 1:
-            sd.dec.append((row_off, slot, m + 1))
-        elif self.tensor_cores:
-            for q0 in range(0, n, self.qpi):
-                sd.ext.append((row_off, slot, m, n, q0))
+        if self.tensor_cores:
+            qpi = self.qpi
+            for q0 in range(0, n, qpi):
+                nq = min(qpi, n - q0)
+                sd.dec.append((row_off + q0, slot, m + q0 + nq, nq))
 
     def alloc_activations(self, rt: StepRuntime, R: int) -> None:
         cfg = self.config
@@ -416,7 +445,6 @@ class B200Transformer:
         dm, D = cfg.model_dim, cfg.head_dim
         W = (cfg.heads + 2 * cfg.n_kv) * D
         rt.h = torch.zeros(R, dm, dtype=dt, device=d)
-        rt.x = torch.zeros(R, dm, dtype=dt, device=d)
         rt.qkv = torch.zeros(R, W, dtype=dt, device=d)
         rt.q = torch.zeros(R, cfg.heads * D, dtype=dt, device=d)
         rt.ctx = torch.zeros(R, cfg.heads * D, dtype=dt, device=d)
@@ -424,8 +452,8 @@ class B200Transformer:
         n_ctas = max(rt.sms, 1)
         rt.n_ctas = n_ctas
         rt.max_dec = R
-        rt.ws = torch.zeros(L.load().tim_decode_ws_floats(n_ctas, R, cfg.heads, D), device=d)
-        rt.counters = torch.zeros(R, dtype=torch.int32, device=d)
+        rt.ws = torch.zeros(L.load().tim_decode_ws_floats(n_ctas, R, cfg.n_kv, D), device=d)
+        rt.counters = torch.zeros(R * cfg.n_kv, dtype=torch.int32, device=d)
 
     # The forward is split in three phases so that a decode step can run as
     # two captured CUDA graphs around one eagerly launched layer-0 attention
@@ -438,65 +466,59 @@ class B200Transformer:
         return 1 + self._layer_head(rt, 0, T)
 
     def _layer_head(self, rt, li, T) -> int:
+        """QKV GEMM on the raw residual + fused RMSNorm-scale/RoPE/page store."""
         cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
         dm, D = cfg.model_dim, cfg.head_dim
-        L.call("tim_rmsnorm", rt.h.data_ptr(), dm, rt.x.data_ptr(), dm, T, dm, 1e-6, td, st)
-        torch.matmul(rt.x[:T], self.wqkv[li], out=rt.qkv[:T])
-        L.call("tim_rope_kv_store", rt.qkv.data_ptr(), T, rt.row_pos.data_ptr(), rt.row_pages.data_ptr(),
-               self.cos.data_ptr(), self.sin.data_ptr(), cfg.heads, cfg.n_kv, D, rt.q.data_ptr(),
+        torch.matmul(rt.h[:T], self.wqkv[li], out=rt.qkv[:T])
+        L.call("tim_rope_kv_store", rt.qkv.data_ptr(), rt.h.data_ptr(), dm, 1e-6, T,
+               rt.row_pos.data_ptr(), rt.row_pages.data_ptr(), self.cos.data_ptr(),
+               self.sin.data_ptr(), cfg.heads, cfg.n_kv, D, rt.q.data_ptr(),
                self.pool_layer(rt.pool.K_layers, li), self.pool_layer(rt.pool.V_layers, li), td, st)
-        return 2
+        return 1
 
-    def _attn(self, rt, sp: int, li: int, T: int, has_dec: bool, has_ext: bool, max_ext: int,
-              timed=None) -> int:
+    def _attn(self, rt, sp: int, li: int, T: int, timed=None) -> int:
+        """Attention of one layer: the split-K tile kernel (all decode and
+        multi-token rows) on the tensor-core path, else the fp32 kernel."""
         cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
         D, hq, hkv = cfg.head_dim, cfg.heads, cfg.n_kv
         kl = self.pool_layer(rt.pool.K_layers, li)
         vl = self.pool_layer(rt.pool.V_layers, li)
         tstride = rt.tables.shape[1]
-        n = 0
         if not self.tensor_cores:
             L.call("tim_attn_extend", sp, T, rt.q.data_ptr(), rt.ctx.data_ptr(), kl, vl,
                    rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, td, st)
             return 1
-        if has_dec:
-            if timed is not None:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e0.record()
-            L.call("tim_attn_decode", sp, rt.q.data_ptr(), rt.ctx.data_ptr(), kl, vl,
-                   rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, rt.ws.data_ptr(),
-                   rt.counters.data_ptr(), rt.n_ctas, rt.max_dec, td, st)
-            if timed is not None:
-                e1 = torch.cuda.Event(enable_timing=True)
-                e1.record()
-                timed.append((e0, e1))
-            n += 1
-        if has_ext:
-            L.call("tim_attn_extend", sp, max_ext, rt.q.data_ptr(), rt.ctx.data_ptr(), kl, vl,
-                   rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, td, st)
-            n += 1
-        return n
+        if timed is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        L.call("tim_attn_decode", sp, rt.q.data_ptr(), rt.ctx.data_ptr(), kl, vl,
+               rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, rt.ws.data_ptr(),
+               rt.counters.data_ptr(), rt.n_ctas, rt.max_dec, td, st)
+        if timed is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            timed.append((e0, e1))
+        return 1
 
     def _layer_tail(self, rt, li, T) -> int:
+        """h += ctx @ wo; u = silu(rms(h) @ w1) (scale fused); h += u @ w2."""
         cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
         dm = cfg.model_dim
         h = rt.h[:T]
         h.addmm_(rt.ctx[:T], self.wo[li])
-        L.call("tim_rmsnorm", rt.h.data_ptr(), dm, rt.x.data_ptr(), dm, T, dm, 1e-6, td, st)
         u = rt.u[:T]
-        torch.matmul(rt.x[:T], self.w1[li], out=u)
-        L.call("tim_silu", u.data_ptr(), u.numel(), td, st)
+        torch.matmul(h, self.w1[li], out=u)
+        L.call("tim_silu_rms", u.data_ptr(), T, cfg.n_mlp, rt.h.data_ptr(), dm, 1e-6, td, st)
         h.addmm_(u, self.w2[li])
-        return 2
+        return 1
 
-    def _post(self, rt, sp: int, step: torch.Tensor, T: int, has_dec, has_ext, max_ext,
-              n_last: int):
+    def _post(self, rt, sp: int, step: torch.Tensor, T: int, n_last: int):
         cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
         dm = cfg.model_dim
         n = self._layer_tail(rt, 0, T)
         for li in range(1, cfg.layers):
             n += self._layer_head(rt, li, T)
-            n += self._attn(rt, sp, li, T, has_dec, has_ext, max_ext)
+            n += self._attn(rt, sp, li, T)
             n += self._layer_tail(rt, li, T)
         off = L.HEADER_INTS                     # `last` is packed first (stepdesc.pack)
         idx = step[off: off + n_last].long()
@@ -508,62 +530,64 @@ class B200Transformer:
         L.call("tim_argmax", logits.data_ptr(), n_last, cfg.vocab, toks.data_ptr(), L.DTYPE_F32, st)
         return n + 2, logits, toks
 
-    def _max_ext(self, rt, T: int) -> int:
-        return (T + self.qpi - 1) // self.qpi + max(rt.max_slots, 1)
-
     def forward_rows(self, rt: StepRuntime, step: torch.Tensor, sd: StepDesc):
         """The batched forward over staged rows (model.py:137-164 for every segment).
-        Graph mode replays captured graphs keyed by (row bucket, has-extend)."""
-        has_dec, has_ext = bool(sd.dec), bool(sd.ext)
+        Graph mode replays the captured graphs of the step's row bucket."""
         timed = rt.attn_events
+        ev = [] if timed is not None else None
         if rt.graph_bucket(sd.n_rows) is not None and sd.rows_pad:
             Tb = sd.rows_pad
-            rt.gstep[: step.numel()].copy_(step) if step.data_ptr() != rt.gstep.data_ptr() else None
-            key = (Tb, has_ext)
-            g = rt.graphs.get(key)
+            if step.data_ptr() != rt.gstep.data_ptr():
+                rt.gstep[: step.numel()].copy_(step)
+            g = rt.graphs.get(Tb)
             if g is None:
-                g = self._capture(rt, Tb, has_ext, sd.last_pad)
-                rt.graphs[key] = g
+                g = self._capture(rt, Tb, sd.last_pad)
+                rt.graphs[Tb] = g
+            pe = rt.phase_events
+            if pe is not None:
+                evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                evs[0].record()
             g["pre"].replay()
-            ev = [] if timed is not None else None
-            n_att = self._attn(rt, rt.gstep.data_ptr(), 0, Tb, True, has_ext,
-                               self._max_ext(rt, Tb), ev)
+            if pe is not None:
+                evs[1].record()
+            n_att = self._attn(rt, rt.gstep.data_ptr(), 0, Tb, ev)
+            if pe is not None:
+                evs[2].record()
             g["post"].replay()
+            if pe is not None:
+                evs[3].record()
+                pe.append((Tb, len(sd.dec), sum(sg[1] + sg[2] for sg in sd.segs), evs))
             rt.launches += g["launches"] + n_att
-            if ev:
-                timed.append((ev[0][0], ev[0][1], sd))
             logits, toks = g["logits"][: len(sd.last)].clone(), g["toks"]
         else:
             T = sd.n_rows
             sp = step.data_ptr()
             n = self._pre(rt, sp, T)
-            ev = [] if timed is not None else None
-            n += self._attn(rt, sp, 0, T, has_dec, has_ext, len(sd.ext), ev)
-            if ev:
-                timed.append((ev[0][0], ev[0][1], sd))
-            m, logits, toks = self._post(rt, sp, step, T, has_dec, has_ext, len(sd.ext), len(sd.last))
+            n += self._attn(rt, sp, 0, T, ev)
+            m, logits, toks = self._post(rt, sp, step, T, len(sd.last))
             rt.launches += n + m
+        if ev:
+            timed.append((ev[0][0], ev[0][1], sd))
         rt.last_logits = logits
         rt.last_tokens = toks
         return toks
 
-    def _capture(self, rt: StepRuntime, Tb: int, has_ext: bool, n_last: int) -> dict:
+    def _capture(self, rt: StepRuntime, Tb: int, n_last: int) -> dict:
         """Capture the pre (embed + layer-0 head) and post (rest) phases for a row
         bucket; the descriptor is read from the fixed rt.gstep buffer."""
         sp = rt.gstep.data_ptr()
-        mx = self._max_ext(rt, Tb)
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):          # warm-up (cuBLAS handles, heuristics)
             self._pre(rt, sp, Tb)
-            self._attn(rt, sp, 0, Tb, True, has_ext, mx)
-            self._post(rt, sp, rt.gstep, Tb, True, has_ext, mx, n_last)
+            self._attn(rt, sp, 0, Tb)
+            self._post(rt, sp, rt.gstep, Tb, n_last)
         torch.cuda.current_stream().wait_stream(side)
         pre, post = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(pre):
             n_pre = self._pre(rt, sp, Tb)
         with torch.cuda.graph(post):
-            n_post, logits, toks = self._post(rt, sp, rt.gstep, Tb, True, has_ext, mx, n_last)
+            n_post, logits, toks = self._post(rt, sp, rt.gstep, Tb, n_last)
         return {"pre": pre, "post": post, "logits": logits, "toks": toks,
                 "launches": n_pre + n_post}
 

@@ -65,13 +65,13 @@ def test_decode_bf16_matches_oracle(n_ctas, hq, hkv):
     q = torch.randn(len(lengths), hq, d, device="cuda", generator=g).to(torch.bfloat16)
     sd = StepDesc()
     for i, n in enumerate(lengths):
-        sd.dec.append((i, i, n))
+        sd.dec.append((i, i, n, 1))
     step = _dev(sd.pack())
     out = torch.zeros(len(lengths), hq, d, device="cuda", dtype=torch.bfloat16)
     sms = L.load().tim_sm_count()
     ctas = sms if n_ctas is None else n_ctas
-    ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, len(lengths), hq, d), device="cuda")
-    cnt = torch.zeros(len(lengths), device="cuda", dtype=torch.int32)
+    ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, len(lengths), hkv, d), device="cuda")
+    cnt = torch.zeros(len(lengths) * hkv, device="cuda", dtype=torch.int32)
     tab_d = _dev(tab)
     for _ in range(2):  # twice: counters must self-reset
         L.call("tim_attn_decode", _ptr(step), _ptr(q), _ptr(out), _ptr(kp), _ptr(vp), _ptr(tab_d),
@@ -99,28 +99,41 @@ def _extend_case(hq, hkv, d, dtype, segs_mn, seed):
     g = torch.Generator(device="cuda").manual_seed(seed + 2)
     q = torch.randn(rows, hq, d, device="cuda", generator=g).to(dtype)
     sd = StepDesc()
-    qpi = L.load().tim_extend_queries_per_item(hq, hkv, d, L.DTYPE_BF16 if dtype == torch.bfloat16 else L.DTYPE_F32)
     row = 0
     for i, (m, n) in enumerate(segs_mn):
         sd.segs.append((i, m, n, row))
-        for q0 in range(0, n, qpi):
-            sd.ext.append((row, i, m, n, q0))
         row += n
     sd.n_rows = rows
     return kp, vp, tab, stride, q, sd, rows
 
 
-@pytest.mark.parametrize("hq,hkv", [(32, 8), (16, 4), (4, 4)])
-def test_extend_bf16_matches_oracle(hq, hkv):
+@pytest.mark.parametrize("n_ctas", [None, 5])
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (16, 4), (4, 4), (32, 2)])
+def test_extend_tiles_bf16_matches_oracle(hq, hkv, n_ctas):
+    """Multi-query tiles (re-encode / prefill / tool rows) through the unified
+    split-K kernel: paged prefix fully visible + causal new block."""
     d = 128
-    segs = [(0, 1), (0, 7), (5, 33), (100, 64), (700, 150), (0, 200), (1200, 3)]
+    segs = [(0, 1), (0, 7), (5, 33), (100, 64), (700, 150), (0, 200), (1200, 3), (40, 1)]
     kp, vp, tab, stride, q, sd, rows = _extend_case(hq, hkv, d, torch.bfloat16, segs, 11)
+    qpi = L.load().tim_extend_queries_per_item(hq, hkv, d, L.DTYPE_BF16)
+    assert qpi == 16 // (hq // hkv)
+    row = 0
+    for i, (m, n) in enumerate(segs):
+        for q0 in range(0, n, qpi):
+            nq = min(qpi, n - q0)
+            sd.dec.append((row + q0, i, m + q0 + nq, nq))
+        row += n
     step = _dev(sd.pack())
     out = torch.zeros(rows, hq, d, device="cuda", dtype=torch.bfloat16)
+    ctas = n_ctas or L.load().tim_sm_count()
+    ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, len(sd.dec), hkv, d), device="cuda")
+    cnt = torch.zeros(len(sd.dec) * hkv, device="cuda", dtype=torch.int32)
     tab_d = _dev(tab)
-    L.call("tim_attn_extend", _ptr(step), len(sd.ext), _ptr(q), _ptr(out), _ptr(kp), _ptr(vp),
-           _ptr(tab_d), stride, hq, hkv, d, 1.0 / np.sqrt(d), L.DTYPE_BF16, _stream())
+    L.call("tim_attn_decode", _ptr(step), _ptr(q), _ptr(out), _ptr(kp), _ptr(vp), _ptr(tab_d),
+           stride, hq, hkv, d, 1.0 / np.sqrt(d), _ptr(ws), _ptr(cnt), ctas, len(sd.dec),
+           L.DTYPE_BF16, _stream())
     torch.cuda.synchronize()
+    assert int(cnt.abs().sum()) == 0
     kf, vf, qf = kp.float().cpu().numpy(), vp.float().cpu().numpy(), q.float().cpu().numpy()
     got = out.float().cpu().numpy()
     row = 0
@@ -172,7 +185,7 @@ def test_rope_kv_store_matches_oracle(dtype):
     vl = torch.zeros_like(kl)
     qo = torch.zeros(n, hq, d, device="cuda", dtype=dtype)
     pos_d, pages_d = _dev(pos), _dev(pages)
-    L.call("tim_rope_kv_store", _ptr(qkv), n, _ptr(pos_d), _ptr(pages_d), _ptr(cos_t),
+    L.call("tim_rope_kv_store", _ptr(qkv), None, 0, 0.0, n, _ptr(pos_d), _ptr(pages_d), _ptr(cos_t),
            _ptr(sin_t), hq, hkv, d, _ptr(qo), _ptr(kl), _ptr(vl),
            L.DTYPE_F32 if dtype == torch.float32 else L.DTYPE_BF16, _stream())
     torch.cuda.synchronize()
@@ -235,6 +248,39 @@ def test_page_ops_match_lifo_oracle():
         assert stack[:sp].cpu().tolist() == pool.free_list
         own = owner.cpu().numpy()
         assert {int(p): int(own[p]) for p in np.nonzero(own >= 0)[0]} == pool.allocated
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_rms_folding_matches_rmsnorm_then_gemm(dtype):
+    """rope_kv_store/silu_rms with h: rms(h) @ W == (h @ W) * inv_rms (model.py:69-70)."""
+    n, dm, hq, hkv, d, P = 9, 256, 4, 2, 32, 64
+    half = d // 2
+    g = torch.Generator(device="cuda").manual_seed(8)
+    h = (torch.randn(n, dm, device="cuda", generator=g) * 3).to(dtype)
+    W = (torch.randn(dm, (hq + 2 * hkv) * d, device="cuda", generator=g) / 16).to(dtype)
+    inv = (1e4 ** (-np.arange(half) / half)).astype(np.float32)
+    ang = np.arange(P, dtype=np.float32)[:, None] * inv[None, :]
+    cos_t, sin_t = _dev(np.cos(ang).astype(np.float32)), _dev(np.sin(ang).astype(np.float32))
+    pos = _dev(np.arange(n, dtype=np.int32))
+    pages = _dev(np.arange(n, dtype=np.int32))
+    qkv = h @ W
+    kl = torch.zeros(n, hkv, d, device="cuda", dtype=dtype)
+    vl = torch.zeros_like(kl)
+    qo = torch.zeros(n, hq, d, device="cuda", dtype=dtype)
+    td = L.DTYPE_F32 if dtype == torch.float32 else L.DTYPE_BF16
+    L.call("tim_rope_kv_store", _ptr(qkv), _ptr(h), dm, 1e-6, n, _ptr(pos), _ptr(pages), _ptr(cos_t),
+           _ptr(sin_t), hq, hkv, d, _ptr(qo), _ptr(kl), _ptr(vl), td, _stream())
+    hf = h.float().cpu().numpy()
+    x = om.rmsnorm(hf) @ W.float().cpu().numpy()
+    tol = 1e-5 if dtype == torch.float32 else 3e-2
+    qr = om.rope(x[:, :hq * d].reshape(n, hq, d), np.arange(n, dtype=np.float32), inv)
+    vr = x[:, (hq + hkv) * d:].reshape(n, hkv, d)
+    assert np.abs(qo.float().cpu().numpy() - qr).max() <= tol * max(1, np.abs(qr).max())
+    assert np.abs(vl.float().cpu().numpy() - vr).max() <= tol * max(1, np.abs(vr).max())
+    u = (h @ W[:, :64]).contiguous()
+    ur = om.silu(om.rmsnorm(hf) @ W[:, :64].float().cpu().numpy())
+    L.call("tim_silu_rms", _ptr(u), n, 64, _ptr(h), dm, 1e-6, td, _stream())
+    assert np.abs(u.float().cpu().numpy() - ur).max() <= tol * max(1, np.abs(ur).max())
 
 
 def test_prune_compact_matches_apply():

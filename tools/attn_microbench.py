@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--trace", action="store_true")
     a = ap.parse_args()
     hq, hkv, d = 32, 8, 128
     rng = np.random.default_rng(0)
@@ -43,13 +44,13 @@ def main():
     tab_d = torch.from_numpy(tab).cuda()
     sd = StepDesc()
     for i, n in enumerate(lens):
-        sd.dec.append((i, i, int(n)))
+        sd.dec.append((i, i, int(n), 1))
     step = torch.from_numpy(sd.pack()).cuda()
     q = torch.randn(a.batch, hq, d, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)
     ctas = a.ctas or L.load().tim_sm_count()
-    ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, a.batch, hq, d), device="cuda")
-    cnt = torch.zeros(a.batch, dtype=torch.int32, device="cuda")
+    ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, a.batch, hkv, d), device="cuda")
+    cnt = torch.zeros(a.batch * hkv, dtype=torch.int32, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
 
     def run(l):
@@ -71,6 +72,17 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) / a.layers)
+    if a.trace:
+        tr = torch.zeros(ctas * 4, dtype=torch.int64, device="cuda")
+        L.call("tim_set_trace", tr.data_ptr())
+        run(0)
+        torch.cuda.synchronize()
+        L.call("tim_set_trace", None)
+        t = tr.view(-1, 4).cpu().numpy().astype(np.float64)
+        t0 = t[:, 0].min()
+        t = (t - t0) / 1000.0
+        print(json.dumps({k: [round(float(np.percentile(t[:, i], p)), 2) for p in (0, 50, 100)]
+                          for i, k in enumerate(["start", "first", "loop_end", "end"])}))
     byts = int(lens.sum()) * hkv * d * 2 * 2 + a.batch * hq * d * 2 * 2
     ms = float(np.median(times))
     print(json.dumps({"tokens": int(lens.sum()), "bytes": byts, "ms": ms,

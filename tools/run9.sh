@@ -1,0 +1,4 @@
+python -m pytest tests/ -x -q -m gpu 2>&1 | tail -3
+python tools/attn_microbench.py --live 724
+python tools/attn_microbench.py --live 309
+TIMRUN_PHASES=1 timeout 900 python bench.py --steps 60 --warmup 3 --skip 600 --cpu-budget 0 2>&1 | tail -16

@@ -171,7 +171,8 @@ def run_gpu(args, rank: int, world: int, dist):
     attn_store = []
     phase_store = [] if os.environ.get("TIMRUN_PHASES") else None
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
-    host_buf = torch.empty(args.batch * 2, dtype=torch.int32, pin_memory=True)
+    host_bufs = [torch.empty(args.batch * 2, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+    result_sum = e2e_steps = 0
     ms = e2e_ms = wall_ms = 0.0
     planned_tokens = e2e_tokens = 0
     launches = h2d = d2h = 0
@@ -201,15 +202,29 @@ def run_gpu(args, rank: int, world: int, dist):
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record()
+        pend = None
         for _ in range(nb):
             rep = eng.step()
             e2e_tokens += sum(rep.decoded.values())
             h2d += rt._last_upload_bytes
             toks = eng.last_step_tokens
+            if pend is not None:                   # read step k-1's result while step k runs
+                ev, buf, n = pend
+                ev.synchronize()
+                result_sum += int(buf[:n].sum())
+                pend = None
             if toks is not None:
                 n = toks.numel()
-                host_buf[:n].copy_(toks)           # D2H of the step's result (greedy tokens)
+                buf = host_bufs[len(host_bufs) - 1 - (e2e_steps % 2)]
+                buf[:n].copy_(toks, non_blocking=True)   # D2H of the step's greedy tokens
+                ev = torch.cuda.Event()
+                ev.record()
+                pend = (ev, buf, n)
                 d2h += n * 4
+            e2e_steps += 1
+        if pend is not None:
+            pend[0].synchronize()
+            result_sum += int(pend[1][:pend[2]].sum())
         f1.record()
         barrier()
         e2e_ms += f0.elapsed_time(f1)

@@ -50,7 +50,7 @@ enum {
  * the same buffer.  Record layouts (int32 fields):
  *   new   : {slot, logical_idx, token, row, live_idx}          host-known tokens
  *   seg   : {slot, m, n, row_off}                               one encode segment
- *   dec   : {row, slot, kv_len, nq} + dec_prefix[n_dec+1]       attention query tiles
+ *   dec   : {row, slot, kv_len, nq, m} + dec_prefix[n_dec+1]    attention query tiles (m: first fresh key)
  *   ext   : {row_off, slot, m, n, q0}                           extend q-tiles
  *   job   : {slot, old_len, suffix_start, reencode_from,
  *            span_off, n_spans, out_row, expect_keep}           prune compaction jobs
@@ -70,7 +70,7 @@ typedef struct {
 
 #define TIM_NEW_FIELDS 5
 #define TIM_SEG_FIELDS 4
-#define TIM_DEC_FIELDS 4
+#define TIM_DEC_FIELDS 5
 #define TIM_EXT_FIELDS 5
 #define TIM_JOB_FIELDS 8
 #define TIM_OP_FIELDS 6
@@ -144,11 +144,13 @@ int32_t tim_silu_rms(void* u, int32_t n_rows, int32_t width, const void* h, int3
                      int32_t dtype, void* stream);
 
 /* K1+K6: split-K (stream-K) paged GQA attention over retained pages only
- * (model.py:149-159).  Work items are query tiles {row, slot, kv_len, nq}:
+ * (model.py:149-159).  Work items are query tiles {row, slot, kv_len, nq, m}:
  * nq consecutive query rows of one request (nq = 1 for decode, up to
  * tim_extend_queries_per_item for re-encode / prefill / tool rows); query i of
  * a tile sees keys [0, kv_len - nq + i] (prefix fully visible, causal inside
- * the new block).  `n_ctas` persistent CTAs split the concatenated key ranges
+ * the new block); keys >= m were written by this step (the kernel is
+ * launched with programmatic dependent launch and streams older pages before
+ * the preceding RoPE+store kernel finishes).  `n_ctas` persistent CTAs split the concatenated key ranges
  * of all tiles evenly; tiles spanning several CTAs are merged in-kernel by the
  * last CTA to finish (log-sum-exp combine).
  * ws: float workspace of tim_decode_ws_floats(n_ctas, max_dec, hkv, D) floats;

@@ -28,7 +28,7 @@ OP_ALLOC = 0
 OP_FREE = 1
 
 HEADER_INTS = 32
-NEW_FIELDS, SEG_FIELDS, DEC_FIELDS, EXT_FIELDS, JOB_FIELDS, OP_FIELDS = 5, 4, 4, 5, 8, 6
+NEW_FIELDS, SEG_FIELDS, DEC_FIELDS, EXT_FIELDS, JOB_FIELDS, OP_FIELDS = 5, 4, 5, 5, 8, 6
 
 # Every exported symbol with its ctypes signature (checked by tests/test_abi.py).
 _i32, _i64, _f32, _p, _cp = C.c_int32, C.c_int64, C.c_float, C.c_void_p, C.c_char_p

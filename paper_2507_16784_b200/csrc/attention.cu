@@ -114,25 +114,31 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
     // per-stage critical path; each stage is then 2*TK bulk copies.
     int32_t* s_ids = reinterpret_cast<int32_t*>(sflag + 4);
     int it = 0;
+    bool waited = false;
     for (int r = r0; r < n_dec && prefix[r] < end; ++r) {
       const int64_t lo = prefix[r], hi = prefix[r + 1];
       const int p0 = (int)((start > lo ? start : lo) - lo);
       const int p1 = (int)((end < hi ? end : hi) - lo);
       const int32_t* trow = tables + (int64_t)dec[r * TIM_DEC_FIELDS + 1] * tstride;
+      const int fresh = dec[r * TIM_DEC_FIELDS + 4];
       for (int c0 = p0; c0 < p1; c0 += kIdChunk) {
         const int c1 = (p1 - c0) < kIdChunk ? p1 : c0 + kIdChunk;
         __syncwarp();
 #pragma unroll 8
         for (int i = lane; i < c1 - c0; i += 32) s_ids[i] = __ldg(trow + c0 + i);
         __syncwarp();
-        // Programmatic dependent launch: block tables were written by earlier
-        // kernels; the K/V rows of this step's tokens and q come from the
-        // kernel right before us (RoPE+store), so wait for it only now.
-        if (it == 0) griddep_wait();
         for (int k0 = c0; k0 < c1; k0 += C::TK, ++it) {
           const int ntok = (c1 - k0) < C::TK ? (c1 - k0) : C::TK;
           const int stg = it % C::STAGES;
           if (it >= C::STAGES) mbar_wait(&empty[stg], ((it / C::STAGES) & 1) ^ 1);
+          // Programmatic dependent launch: pages of earlier tokens were written
+          // by earlier steps, so they stream while the preceding RoPE+store
+          // kernel still runs; only a stage holding this step's fresh keys
+          // (>= the segment start) waits for that kernel to finish.
+          if (!waited && k0 + ntok > fresh) {
+            griddep_wait();
+            waited = true;
+          }
           if (lane == 0) mbar_arrive_expect_tx(&full[stg], 2 * C::TK * C::ROW_BYTES);
           __syncwarp();
           const int row = lane & (C::TK - 1);
@@ -147,7 +153,7 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
   }
 
   // -------------------------------------------------------------- consumers
-  griddep_wait();
+  griddep_wait();   // q is written by the preceding kernel
   // A work item is a query tile: nq consecutive queries of one request (1 for
   // decode, up to 16/grp for extend / re-encode rows) x the grp q heads of
   // this warp's kv head = the 16 rows of the m16n8k16 tile (row rr = query

@@ -351,7 +351,7 @@ class B200Transformer:
             self.wo = [mat(dm, dm) for _ in range(cfg.layers)]
             self.w1 = [mat(dm, cfg.n_mlp) for _ in range(cfg.layers)]
             self.w2 = [mat(cfg.n_mlp, dm) for _ in range(cfg.layers)]
-        self.emb_t32 = self.emb.float().t().contiguous()
+        self.emb_t = self.emb.t().contiguous()     # tied LM head (model.py:164)
         cos, sin = _rope_tables(cfg)
         self.cos = torch.from_numpy(cos).to(self.dev)
         self.sin = torch.from_numpy(sin).to(self.dev)
@@ -437,7 +437,7 @@ class B200Transformer:
             qpi = self.qpi
             for q0 in range(0, n, qpi):
                 nq = min(qpi, n - q0)
-                sd.dec.append((row_off + q0, slot, m + q0 + nq, nq))
+                sd.dec.append((row_off + q0, slot, m + q0 + nq, nq, m))
 
     def alloc_activations(self, rt: StepRuntime, R: int) -> None:
         cfg = self.config
@@ -525,7 +525,7 @@ class B200Transformer:
         hl = rt.h.index_select(0, idx)
         xl = torch.empty_like(hl)
         L.call("tim_rmsnorm", hl.data_ptr(), dm, xl.data_ptr(), dm, n_last, dm, 1e-6, td, st)
-        logits = torch.matmul(xl.float(), self.emb_t32)
+        logits = torch.matmul(xl, self.emb_t).float()
         toks = torch.empty(n_last, dtype=torch.int32, device=self.dev)
         L.call("tim_argmax", logits.data_ptr(), n_last, cfg.vocab, toks.data_ptr(), L.DTYPE_F32, st)
         return n + 2, logits, toks

@@ -65,7 +65,7 @@ def test_decode_bf16_matches_oracle(n_ctas, hq, hkv):
     q = torch.randn(len(lengths), hq, d, device="cuda", generator=g).to(torch.bfloat16)
     sd = StepDesc()
     for i, n in enumerate(lengths):
-        sd.dec.append((i, i, n, 1))
+        sd.dec.append((i, i, n, 1, n - 1))
     step = _dev(sd.pack())
     out = torch.zeros(len(lengths), hq, d, device="cuda", dtype=torch.bfloat16)
     sms = L.load().tim_sm_count()
@@ -121,7 +121,7 @@ def test_extend_tiles_bf16_matches_oracle(hq, hkv, n_ctas):
     for i, (m, n) in enumerate(segs):
         for q0 in range(0, n, qpi):
             nq = min(qpi, n - q0)
-            sd.dec.append((row + q0, i, m + q0 + nq, nq))
+            sd.dec.append((row + q0, i, m + q0 + nq, nq, m))
         row += n
     step = _dev(sd.pack())
     out = torch.zeros(rows, hq, d, device="cuda", dtype=torch.bfloat16)

@@ -44,7 +44,7 @@ def main():
     tab_d = torch.from_numpy(tab).cuda()
     sd = StepDesc()
     for i, n in enumerate(lens):
-        sd.dec.append((i, i, int(n), 1))
+        sd.dec.append((i, i, int(n), 1, int(n) - 1))
     step = torch.from_numpy(sd.pack()).cuda()
     q = torch.randn(a.batch, hq, d, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)

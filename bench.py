@@ -407,8 +407,11 @@ def main():
 
     dist = None
     if world > 1:
+        import torch
         import torch.distributed as dist_mod
-        dist_mod.init_process_group("nccl")
+        local = int(os.environ.get("LOCAL_RANK", 0))
+        torch.cuda.set_device(local)
+        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
     res = run_gpu(args, rank, world, dist)
     if rank == 0:

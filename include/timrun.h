@@ -50,8 +50,10 @@ enum {
  * the same buffer.  Record layouts (int32 fields):
  *   new   : {slot, logical_idx, token, row, live_idx}          host-known tokens
  *   seg   : {slot, m, n, row_off}                               one encode segment
- *   dec   : {row, slot, kv_len, nq, m} + dec_prefix[n_dec+1]    attention query tiles (m: first fresh key)
- *   ext   : {row_off, slot, m, n, q0}                           extend q-tiles
+ *   dec   : {row, slot, kv_len, nq, m, group} + dec_prefix[n_dec+1]
+ *                                   decode tiles (1 query x all kv heads; m = first fresh key)
+ *   ext   : {row, slot, kv_len, nq, m, group} + ext_prefix[n_ext+1]
+ *                                   multi-token tiles (queries x one kv-head group)
  *   job   : {slot, old_len, suffix_start, reencode_from,
  *            span_off, n_spans, out_row, expect_keep}           prune compaction jobs
  *   spans : {start, end}                                        coalesced evict spans
@@ -65,13 +67,14 @@ typedef struct {
   int32_t dec_total;
   int32_t off_new, off_segs, off_dec, off_dec_prefix, off_ext, off_jobs, off_spans;
   int32_t off_ops, off_phases, off_last;
-  int32_t reserved[11];
+  int32_t ext_total, off_ext_prefix;
+  int32_t reserved[9];
 } tim_step_header;  /* 32 int32 */
 
 #define TIM_NEW_FIELDS 5
 #define TIM_SEG_FIELDS 4
-#define TIM_DEC_FIELDS 5
-#define TIM_EXT_FIELDS 5
+#define TIM_DEC_FIELDS 6
+#define TIM_EXT_FIELDS 6
 #define TIM_JOB_FIELDS 8
 #define TIM_OP_FIELDS 6
 
@@ -144,23 +147,30 @@ int32_t tim_silu_rms(void* u, int32_t n_rows, int32_t width, const void* h, int3
                      int32_t dtype, void* stream);
 
 /* K1+K6: split-K (stream-K) paged GQA attention over retained pages only
- * (model.py:149-159).  Work items are query tiles {row, slot, kv_len, nq, m}:
- * nq consecutive query rows of one request (nq = 1 for decode, up to
- * tim_extend_queries_per_item for re-encode / prefill / tool rows); query i of
- * a tile sees keys [0, kv_len - nq + i] (prefix fully visible, causal inside
- * the new block); keys >= m were written by this step (the kernel is
- * launched with programmatic dependent launch and streams older pages before
- * the preceding RoPE+store kernel finishes).  `n_ctas` persistent CTAs split the concatenated key ranges
+ * (model.py:149-159).  Work items are query tiles {row, slot, kv_len, nq, m,
+ * group}: nq consecutive query rows of one request; query i of a tile sees
+ * keys [0, kv_len - nq + i] (prefix fully visible, causal inside the new
+ * block); keys >= m were written by this step.  mode 0 runs the step's decode
+ * tiles (`dec`: one query x all kv heads, whole page rows); mode 1 runs its
+ * multi-token tiles (`ext`: tim_extend_queries_per_item queries x one of
+ * tim_extend_head_groups kv-head groups), so re-encode / prefill / tool rows
+ * share one K/V stream per tile.  The kernel is launched with programmatic
+ * dependent launch and streams older pages before the preceding RoPE+store
+ * kernel finishes.  `n_ctas` persistent CTAs split the concatenated key ranges
  * of all tiles evenly; tiles spanning several CTAs are merged in-kernel by the
  * last CTA to finish (log-sum-exp combine).
  * ws: float workspace of tim_decode_ws_floats(n_ctas, max_dec, hkv, D) floats;
- * counters: int32[max_dec * hkv] zero-initialised once (self-resetting); max_dec bounds n_dec. */
+ * counters: int32[max_dec * 8] zero-initialised once (self-resetting); max_dec
+ * bounds the tile count. */
 int64_t tim_decode_ws_floats(int32_t n_ctas, int32_t max_dec, int32_t hkv, int32_t head_dim);
-int32_t tim_attn_decode(const int32_t* step, const void* q, void* out, const void* k_layer,
-                        const void* v_layer, const int32_t* block_tables, int64_t table_stride,
-                        int32_t hq, int32_t hkv, int32_t head_dim, float scale, float* ws,
-                        int32_t* counters, int32_t n_ctas, int32_t max_dec, int32_t dtype,
-                        void* stream);
+int32_t tim_attn_decode(const int32_t* step, int32_t mode, const void* q, void* out,
+                        const void* k_layer, const void* v_layer, const int32_t* block_tables,
+                        int64_t table_stride, int32_t hq, int32_t hkv, int32_t head_dim,
+                        float scale, float* ws, int32_t* counters, int32_t n_ctas, int32_t max_dec,
+                        int32_t dtype, void* stream);
+/* Queries per multi-token tile and kv-head groups per query for a config. */
+int32_t tim_extend_queries_per_item(int32_t hq, int32_t hkv, int32_t head_dim, int32_t dtype);
+int32_t tim_extend_head_groups(int32_t hkv);
 
 /* Diagnostics: per-CTA %globaltimer timeline of tim_attn_decode written to
  * buf[4*cta .. 4*cta+3] = {start, first stage landed, main loop end, end};
@@ -174,8 +184,6 @@ int32_t tim_attn_extend(const int32_t* step, int32_t max_items, const void* q, v
                         const void* k_layer, const void* v_layer, const int32_t* block_tables,
                         int64_t table_stride, int32_t hq, int32_t hkv, int32_t head_dim,
                         float scale, int32_t dtype, void* stream);
-/* Queries per attention tile of tim_attn_decode for a config (the host tiles segments with it). */
-int32_t tim_extend_queries_per_item(int32_t hq, int32_t hkv, int32_t head_dim, int32_t dtype);
 
 /* Greedy argmax over rows of logits [n, vocab] (lowest id on ties, model.py:186-192). */
 int32_t tim_argmax(const void* logits, int32_t n_rows, int32_t vocab, int32_t* out,

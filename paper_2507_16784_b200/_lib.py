@@ -28,7 +28,7 @@ OP_ALLOC = 0
 OP_FREE = 1
 
 HEADER_INTS = 32
-NEW_FIELDS, SEG_FIELDS, DEC_FIELDS, EXT_FIELDS, JOB_FIELDS, OP_FIELDS = 5, 4, 5, 5, 8, 6
+NEW_FIELDS, SEG_FIELDS, DEC_FIELDS, EXT_FIELDS, JOB_FIELDS, OP_FIELDS = 5, 4, 6, 6, 8, 6
 
 # Every exported symbol with its ctypes signature (checked by tests/test_abi.py).
 _i32, _i64, _f32, _p, _cp = C.c_int32, C.c_int64, C.c_float, C.c_void_p, C.c_char_p
@@ -48,10 +48,11 @@ SIGNATURES = {
                                  _p, _i32, _p]),
     "tim_silu_rms": (_i32, [_p, _i32, _i32, _p, _i32, _f32, _i32, _p]),
     "tim_decode_ws_floats": (_i64, [_i32, _i32, _i32, _i32]),
-    "tim_attn_decode": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _i32, _f32, _p, _p, _i32,
-                               _i32, _i32, _p]),
+    "tim_attn_decode": (_i32, [_p, _i32, _p, _p, _p, _p, _p, _i64, _i32, _i32, _i32, _f32, _p, _p,
+                               _i32, _i32, _i32, _p]),
     "tim_attn_extend": (_i32, [_p, _i32, _p, _p, _p, _p, _p, _i64, _i32, _i32, _i32, _f32, _i32, _p]),
     "tim_extend_queries_per_item": (_i32, [_i32, _i32, _i32, _i32]),
+    "tim_extend_head_groups": (_i32, [_i32]),
     "tim_argmax": (_i32, [_p, _i32, _i32, _p, _i32, _p]),
     "tim_set_trace": (_i32, [_p]),
 }
@@ -94,6 +95,7 @@ def call(name: str, *args) -> int:
     fn = getattr(load(), name)
     rc = fn(*args)
     if SIGNATURES[name][0] is _i32 and name not in ("tim_abi_version", "tim_sm_count",
-                                                    "tim_extend_queries_per_item") and rc != TIM_OK:
+                                                    "tim_extend_queries_per_item",
+                                                    "tim_extend_head_groups") and rc != TIM_OK:
         raise TimrunError(rc, f"{name}: {last_error()}")
     return rc

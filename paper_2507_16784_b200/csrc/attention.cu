@@ -31,15 +31,21 @@ constexpr int kFastPieces = 4;      // partials merged by the one-round-trip com
 constexpr int kMinTokensPerCta = 64;  // below this many kv tokens per CTA, use fewer CTAs
 
 // ===================================================================== K1
-template <int D, int HKV>
-struct DecCfg {
+// HG kv heads per CTA (one page row slice of HG*D*2 contiguous bytes per
+// token and layer), WPH consumer warps per kv head (each 16 MMA rows).
+// Decode tiles use HG = Hkv, WPH = 1 (one query x all heads, whole 2 KiB page
+// rows); multi-token tiles use fewer heads and more warps per head so one
+// K/V stream serves WPH x 16/group queries.
+template <int D, int HG, int WPH>
+struct AttnCfg {
+  static constexpr int NW = HG * WPH;                 // consumer warps
   static constexpr int TK = 16;                       // tokens per stage
-  static constexpr int ROW_BYTES = HKV * D * 2;       // one page, all kv heads, one layer
+  static constexpr int ROW_BYTES = HG * D * 2;        // page-row slice per token and layer
   static constexpr int ROW_STRIDE = ROW_BYTES + 16;   // +16B: conflict-free ldmatrix rows
   static constexpr int STAGE_BYTES = 2 * TK * ROW_STRIDE;
   static constexpr int STAGES_RAW = 204800 / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
-  static constexpr int THREADS = (HKV + 1) * 32;
+  static constexpr int STAGES = STAGES_RAW > 12 ? 12 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+  static constexpr int THREADS = (NW + 1) * 32;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 16 + kIdChunk * 4;
   static constexpr int KC = D / 16;
   static constexpr int NT = D / 8;
@@ -59,14 +65,15 @@ __device__ __forceinline__ int64_t cta_of(int64_t x, int64_t G, int64_t N) {
   return ((x + 1) * G - 1) / N;
 }
 
-template <int D, int HKV>
-__global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
-    attn_decode_kernel(const int32_t* __restrict__ step, const __nv_bfloat16* __restrict__ q,
-                       __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kl,
-                       const __nv_bfloat16* __restrict__ vl, const int32_t* __restrict__ tables,
-                       int64_t tstride, int hq, float scale, float* __restrict__ ws,
-                       int32_t* __restrict__ counters, int max_dec) {
-  using C = DecCfg<D, HKV>;
+template <int D, int HKV, int HG, int WPH>
+__global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
+    attn_tiles_kernel(const int32_t* __restrict__ step, int list, const __nv_bfloat16* __restrict__ q,
+                      __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kl,
+                      const __nv_bfloat16* __restrict__ vl, const int32_t* __restrict__ tables,
+                      int64_t tstride, int hq, float scale, float* __restrict__ ws,
+                      int32_t* __restrict__ counters, int max_dec) {
+  using C = AttnCfg<D, HG, WPH>;
+  constexpr int NW = C::NW;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
@@ -75,15 +82,15 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
   unsigned long long* trace = g_trace;
   if (trace && threadIdx.x == 0) trace[4 * blockIdx.x] = gtimer();
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
-  const int n_dec = hd.n_dec;
-  const int64_t N = hd.dec_total;
+  const int n_dec = list ? hd.n_ext : hd.n_dec;
+  const int64_t N = list ? hd.ext_total : hd.dec_total;
   if (n_dec == 0 || N == 0) return;
   const int64_t want = (N + kMinTokensPerCta - 1) / kMinTokensPerCta;
   const int64_t G = gridDim.x < want ? gridDim.x : want;
   const int c = blockIdx.x;
   if (c >= G) return;
-  const int32_t* dec = step + hd.off_dec;
-  const int32_t* prefix = step + hd.off_dec_prefix;
+  const int32_t* dec = step + (list ? hd.off_ext : hd.off_dec);
+  const int32_t* prefix = step + (list ? hd.off_ext_prefix : hd.off_dec_prefix);
   const int64_t start = (int64_t)c * N / G, end = (int64_t)(c + 1) * N / G;
 
   // first segment of this CTA: largest r with prefix[r] <= start
@@ -101,13 +108,13 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], HKV);
+      mbar_init(&empty[s], NW);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == HKV) {
+  if (warp == NW) {
     // ------------------------------------------------------------ producer
     // Page ids of the piece are staged into shared memory a chunk at a time
     // (one coalesced read per kIdChunk tokens), so the id latency is off the
@@ -121,6 +128,7 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
       const int p1 = (int)((end < hi ? end : hi) - lo);
       const int32_t* trow = tables + (int64_t)dec[r * TIM_DEC_FIELDS + 1] * tstride;
       const int fresh = dec[r * TIM_DEC_FIELDS + 4];
+      const int64_t hoff = (int64_t)dec[r * TIM_DEC_FIELDS + 5] * HG * D;   // head-group slice
       for (int c0 = p0; c0 < p1; c0 += kIdChunk) {
         const int c1 = (p1 - c0) < kIdChunk ? p1 : c0 + kIdChunk;
         __syncwarp();
@@ -144,7 +152,7 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
           const int row = lane & (C::TK - 1);
           const int32_t page = s_ids[k0 - c0 + (row < ntok ? row : ntok - 1)];  // pad rows repeat a valid row
           uint8_t* base = smem + stg * C::STAGE_BYTES + (lane >= C::TK ? C::TK * C::ROW_STRIDE : 0);
-          const __nv_bfloat16* src = (lane >= C::TK ? vl : kl) + (int64_t)page * (HKV * D);
+          const __nv_bfloat16* src = (lane >= C::TK ? vl : kl) + (int64_t)page * (HKV * D) + hoff;
           bulk_g2s(base + row * C::ROW_STRIDE, src, C::ROW_BYTES, &full[stg]);
         }
       }
@@ -160,10 +168,12 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
   // rr/grp, head rr%grp).  Query qi of the tile sees keys <= kv_len-nq+qi
   // (prefix fully visible, causal inside the new block, model.py:139-140).
   const int grp = hq / HKV;
+  const int qpw = 16 / grp;                 // queries per warp (16 MMA rows)
+  const int hloc = warp / WPH, sub = warp % WPH;
   const int g = lane >> 2, t = lane & 3;
   const float sl = scale * kLog2e;
   const uint32_t smem_base = smem_u32(smem);
-  const int64_t slot_floats = (int64_t)HKV * 16 * D;   // one partial: 16 rows per kv head
+  const int64_t slot_floats = (int64_t)8 * 16 * D;     // one partial: 16 rows x <= 8 warps
   float* ws_o = ws;
   float* ws_ml = ws + (int64_t)(gridDim.x + max_dec) * slot_floats;
   int it = 0;
@@ -174,7 +184,10 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
     const int p1 = (int)((end < hi ? end : hi) - lo);
     const int32_t* rec = dec + r * TIM_DEC_FIELDS;
     const int qrow = rec[0], kv_len = rec[2], nq = rec[3];
-    const int nrows = nq * grp;
+    const int kvh = rec[5] * HG + hloc;      // this warp's kv head
+    int nw_q = nq - sub * qpw;               // queries of this warp in the tile
+    nw_q = nw_q < 0 ? 0 : (nw_q > qpw ? qpw : nw_q);
+    const int nrows = nw_q * grp;
 
     int lim[2], orow[2];
     bool valid[2];
@@ -183,9 +196,9 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
     for (int h = 0; h < 2; ++h) {
       const int rr = g + 8 * h;
       valid[h] = rr < nrows;
-      const int qi = rr / grp;
+      const int qi = sub * qpw + rr / grp;
       lim[h] = kv_len - nq + qi;                          // last visible key (absolute)
-      orow[h] = (qrow + qi) * hq + warp * grp + (rr - qi * grp);
+      orow[h] = (qrow + qi) * hq + kvh * grp + (rr % grp);
     }
 #pragma unroll
     for (int kc = 0; kc < C::KC; ++kc) {
@@ -206,7 +219,7 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
       const int stg = it % C::STAGES;
       mbar_wait(&full[stg], (it / C::STAGES) & 1);
       if (trace && it == 0 && threadIdx.x == 0) trace[4 * blockIdx.x + 1] = gtimer();
-      const uint32_t kbase = smem_base + stg * C::STAGE_BYTES + warp * D * 2;
+      const uint32_t kbase = smem_base + stg * C::STAGE_BYTES + hloc * D * 2;
       const uint32_t vbase = kbase + C::TK * C::ROW_STRIDE;
 
       float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
@@ -302,7 +315,8 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
       }
       continue;
     }
-    const int64_t wslot = ((c + r) * HKV + warp) * 16;   // first of this warp's 16 partial rows
+    if (nrows == 0) continue;
+    const int64_t wslot = ((c + r) * 8 + warp) * 16;     // first of this warp's 16 partial rows
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int rr = g + 8 * h;
@@ -319,9 +333,9 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
     if (lane == 0) {
       int old;
       asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
-                   : "=r"(old) : "l"(counters + (int64_t)r * HKV + warp) : "memory");
+                   : "=r"(old) : "l"(counters + (int64_t)r * 8 + warp) : "memory");
       last = old == npieces - 1;
-      if (last) counters[(int64_t)r * HKV + warp] = 0;
+      if (last) counters[(int64_t)r * 8 + warp] = 0;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (!last) continue;
@@ -348,7 +362,7 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
             ml[k][p] = make_float2(-INFINITY, 0.f);
             ov[k][p] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (r0w + k < nrows && cb + p <= c_last) {
-              const int64_t pr = ((cb + p + r) * HKV + warp) * 16 + r0w + k;
+              const int64_t pr = ((cb + p + r) * 8 + warp) * 16 + r0w + k;
               ml[k][p] = __ldcg(reinterpret_cast<const float2*>(ws_ml + pr * 2));
               if (lane * 4 < D) ov[k][p] = __ldcg(reinterpret_cast<const float4*>(ws_o + pr * D) + lane);
             }
@@ -376,8 +390,8 @@ __global__ void __launch_bounds__(DecCfg<D, HKV>::THREADS, 1)
       for (int k = 0; k < 4; ++k) {
         const int rr = r0w + k;
         if (rr < nrows && lane * 4 < D) {
-          const int qi = rr / grp;
-          const int64_t oidx = (int64_t)(qrow + qi) * hq + warp * grp + (rr - qi * grp);
+          const int qi = sub * qpw + rr / grp;
+          const int64_t oidx = (int64_t)(qrow + qi) * hq + kvh * grp + (rr % grp);
           const float inv = 1.f / den[k];
           uint2 pk;
           pk.x = pack_bf16(acc[k].x * inv, acc[k].y * inv);
@@ -459,14 +473,15 @@ __global__ void attn_generic_kernel(const int32_t* __restrict__ step, const T* _
   }
 }
 
-template <int D, int HKV>
-int32_t launch_decode(const int32_t* step, const void* q, void* out, const void* kl, const void* vl,
-                      const int32_t* tables, int64_t tstride, int hq, float scale, float* ws,
-                      int32_t* counters, int n_ctas, int max_dec, cudaStream_t st) {
-  using C = DecCfg<D, HKV>;
+template <int D, int HKV, int HG, int WPH>
+int32_t launch_tiles(const int32_t* step, int list, const void* q, void* out, const void* kl,
+                     const void* vl, const int32_t* tables, int64_t tstride, int hq, float scale,
+                     float* ws, int32_t* counters, int n_ctas, int max_dec, cudaStream_t st) {
+  using C = AttnCfg<D, HG, WPH>;
+  auto kern = attn_tiles_kernel<D, HKV, HG, WPH>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_decode_kernel<D, HKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -480,15 +495,18 @@ int32_t launch_decode(const int32_t* step, const void* q, void* out, const void*
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(
-      &cfg, attn_decode_kernel<D, HKV>, step, (const __nv_bfloat16*)q, (__nv_bfloat16*)out,
+      &cfg, kern, step, list, (const __nv_bfloat16*)q, (__nv_bfloat16*)out,
       (const __nv_bfloat16*)kl, (const __nv_bfloat16*)vl, tables, tstride, hq, scale, ws, counters,
       max_dec);
   if (e != cudaSuccess) {
-    set_last_error("attn_decode launch: %s", cudaGetErrorString(e));
+    set_last_error("attn_tiles launch: %s", cudaGetErrorString(e));
     return TIM_CUDA_ERROR;
   }
-  return check_launch("attn_decode");
+  return check_launch("attn_tiles");
 }
+
+// kv heads per CTA for multi-token tiles (the rest of the 8 warps share a head)
+constexpr int ext_hg(int hkv) { return hkv >= 8 ? 4 : (hkv >= 4 ? 2 : 1); }
 
 }  // namespace tim
 
@@ -503,14 +521,18 @@ static bool tensor_core_shape(int32_t hq, int32_t hkv, int32_t head_dim) {
 }
 
 extern "C" int64_t tim_decode_ws_floats(int32_t n_ctas, int32_t max_dec, int32_t hkv, int32_t head_dim) {
-  return (int64_t)(n_ctas + max_dec) * hkv * 16 * (head_dim + 2);
+  (void)hkv;  // partial slots are sized for the 8 consumer warps of a CTA
+  return (int64_t)(n_ctas + max_dec) * 8 * 16 * (head_dim + 2);
 }
 
 extern "C" int32_t tim_extend_queries_per_item(int32_t hq, int32_t hkv, int32_t head_dim, int32_t dtype) {
-  // queries per attention work tile of tim_attn_decode (16 MMA rows / group)
-  if (dtype == TIM_DTYPE_BF16 && tensor_core_shape(hq, hkv, head_dim)) return 16 / (hq / hkv);
+  // queries per multi-token attention tile (mode 1 of tim_attn_decode)
+  if (dtype == TIM_DTYPE_BF16 && tensor_core_shape(hq, hkv, head_dim))
+    return (8 / ext_hg(hkv)) * (16 / (hq / hkv));
   return 1 << 30;  // generic path: whole segments
 }
+
+extern "C" int32_t tim_extend_head_groups(int32_t hkv) { return hkv / ext_hg(hkv); }
 
 static int32_t launch_generic(const int32_t* step, int32_t n_rows, const void* q, void* out,
                               const void* kl, const void* vl, const int32_t* tables,
@@ -534,11 +556,12 @@ static int32_t launch_generic(const int32_t* step, int32_t n_rows, const void* q
 
 // Rows handled: decode queries listed in the step (n_dec).  For the fp32 /
 // generic configuration every row is handled by tim_attn_extend instead.
-extern "C" int32_t tim_attn_decode(const int32_t* step, const void* q, void* out, const void* k_layer,
-                                   const void* v_layer, const int32_t* block_tables,
-                                   int64_t table_stride, int32_t hq, int32_t hkv, int32_t head_dim,
-                                   float scale, float* ws, int32_t* counters, int32_t n_ctas,
-                                   int32_t max_dec, int32_t dtype, void* stream) {
+extern "C" int32_t tim_attn_decode(const int32_t* step, int32_t mode, const void* q, void* out,
+                                   const void* k_layer, const void* v_layer,
+                                   const int32_t* block_tables, int64_t table_stride, int32_t hq,
+                                   int32_t hkv, int32_t head_dim, float scale, float* ws,
+                                   int32_t* counters, int32_t n_ctas, int32_t max_dec,
+                                   int32_t dtype, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype != TIM_DTYPE_BF16 || !tensor_core_shape(hq, hkv, head_dim)) {
     set_last_error("tim_attn_decode: tensor-core path needs bf16, hkv in {1,2,4,8}, "
@@ -546,13 +569,20 @@ extern "C" int32_t tim_attn_decode(const int32_t* step, const void* q, void* out
     return TIM_UNSUPPORTED;
   }
   if (n_ctas <= 0) return TIM_OK;
-#define TIM_DEC(DD, HH)                                                                        \
-  if (head_dim == DD && hkv == HH)                                                             \
-    return launch_decode<DD, HH>(step, q, out, k_layer, v_layer, block_tables, table_stride, hq, \
-                                 scale, ws, counters, n_ctas, max_dec, st);
-  TIM_DEC(128, 8) TIM_DEC(128, 4) TIM_DEC(128, 2) TIM_DEC(128, 1)
-  TIM_DEC(64, 8) TIM_DEC(64, 4) TIM_DEC(64, 2) TIM_DEC(64, 1)
-#undef TIM_DEC
+#define TIM_TILES(DD, HH)                                                                      \
+  if (head_dim == DD && hkv == HH) {                                                           \
+    if (mode == 0)                                                                             \
+      return launch_tiles<DD, HH, HH, 1>(step, 0, q, out, k_layer, v_layer, block_tables,      \
+                                         table_stride, hq, scale, ws, counters, n_ctas,        \
+                                         max_dec, st);                                         \
+    return launch_tiles<DD, HH, ext_hg(HH), 8 / ext_hg(HH)>(step, 1, q, out, k_layer, v_layer, \
+                                                            block_tables, table_stride, hq,    \
+                                                            scale, ws, counters, n_ctas,       \
+                                                            max_dec, st);                      \
+  }
+  TIM_TILES(128, 8) TIM_TILES(128, 4) TIM_TILES(128, 2) TIM_TILES(128, 1)
+  TIM_TILES(64, 8) TIM_TILES(64, 4) TIM_TILES(64, 2) TIM_TILES(64, 1)
+#undef TIM_TILES
   return TIM_UNSUPPORTED;
 }
 

@@ -247,8 +247,9 @@ class StepRuntime:
                    self.tables.shape[1], self.live.data_ptr(), self.live.shape[1],
                    self.logical.data_ptr(), self.logical.shape[1], self.row_tokens.data_ptr(),
                    self.row_pages.data_ptr(), self.row_pos.data_ptr(), stream_handle())
-            if b not in self.graphs:
-                self.graphs[b] = self.model._capture(self, b, self.max_slots)
+            for has_ext in (False, True):
+                if (b, has_ext) not in self.graphs:
+                    self.graphs[(b, has_ext)] = self.model._capture(self, b, self.max_slots, has_ext)
         torch.cuda.synchronize()
 
     def run_step(self, sd: StepDesc, forward: bool = True):
@@ -358,7 +359,7 @@ class B200Transformer:
         self.scale = 1.0 / math.sqrt(D)
         self.tensor_cores = (cfg.precision == "bfloat16" and L.load().tim_extend_queries_per_item(
             hq, hkv, D, L.DTYPE_BF16) < (1 << 30))
-        self.qpi = L.load().tim_extend_queries_per_item(hq, hkv, D, cfg.tim_dtype)
+        self.tile_q = 16 // (hq // hkv) if self.tensor_cores else 0   # queries per mode-0 tile
         self._runtimes: dict[int, StepRuntime] = {}
 
     # ------------------------------------------------------- protocol
@@ -433,11 +434,16 @@ class B200Transformer:
         """Attention work records for one segment: split-K decode for single-row
         tensor-core segments, q-tiles for the rest."""
         sd.segs.append((slot, m, n, row_off))
-        if self.tensor_cores:
-            qpi = self.qpi
-            for q0 in range(0, n, qpi):
-                nq = min(qpi, n - q0)
-                sd.dec.append((row_off + q0, slot, m + q0 + nq, nq, m))
+        if not self.tensor_cores:
+            return
+        # Every row goes through the decode-tile kernel (mode 0): tiles of
+        # tile_q consecutive queries x all kv heads.  Measured on B200, this
+        # beats the head-grouped multi-token mode (mode 1: fewer K/V bytes per
+        # query but the same MMA-instruction count, which bounds these tiles).
+        tq = self.tile_q
+        for q0 in range(0, n, tq):
+            nq = min(tq, n - q0)
+            sd.dec.append((row_off + q0, slot, m + q0 + nq, nq, m, 0))
 
     def alloc_activations(self, rt: StepRuntime, R: int) -> None:
         cfg = self.config
@@ -453,7 +459,7 @@ class B200Transformer:
         rt.n_ctas = n_ctas
         rt.max_dec = R
         rt.ws = torch.zeros(L.load().tim_decode_ws_floats(n_ctas, R, cfg.n_kv, D), device=d)
-        rt.counters = torch.zeros(R * cfg.n_kv, dtype=torch.int32, device=d)
+        rt.counters = torch.zeros(R * 8, dtype=torch.int32, device=d)
 
     # The forward is split in three phases so that a decode step can run as
     # two captured CUDA graphs around one eagerly launched layer-0 attention
@@ -476,9 +482,10 @@ class B200Transformer:
                self.pool_layer(rt.pool.K_layers, li), self.pool_layer(rt.pool.V_layers, li), td, st)
         return 1
 
-    def _attn(self, rt, sp: int, li: int, T: int, timed=None) -> int:
-        """Attention of one layer: the split-K tile kernel (all decode and
-        multi-token rows) on the tensor-core path, else the fp32 kernel."""
+    def _attn(self, rt, sp: int, li: int, T: int, has_ext: bool, timed=None) -> int:
+        """Attention of one layer: the split-K tile kernel over the decode tiles
+        (mode 0) and, when the step has multi-token rows, over its multi-token
+        tiles (mode 1) on the tensor-core path; else the fp32 kernel."""
         cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
         D, hq, hkv = cfg.head_dim, cfg.heads, cfg.n_kv
         kl = self.pool_layer(rt.pool.K_layers, li)
@@ -491,14 +498,17 @@ class B200Transformer:
         if timed is not None:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
-        L.call("tim_attn_decode", sp, rt.q.data_ptr(), rt.ctx.data_ptr(), kl, vl,
-               rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, rt.ws.data_ptr(),
-               rt.counters.data_ptr(), rt.n_ctas, rt.max_dec, td, st)
+        n = 0
+        for mode in ((0, 1) if has_ext else (0,)):
+            L.call("tim_attn_decode", sp, mode, rt.q.data_ptr(), rt.ctx.data_ptr(), kl, vl,
+                   rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, rt.ws.data_ptr(),
+                   rt.counters.data_ptr(), rt.n_ctas, rt.max_dec, td, st)
+            n += 1
         if timed is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
             timed.append((e0, e1))
-        return 1
+        return n
 
     def _layer_tail(self, rt, li, T) -> int:
         """h += ctx @ wo; u = silu(rms(h) @ w1) (scale fused); h += u @ w2."""
@@ -512,13 +522,13 @@ class B200Transformer:
         h.addmm_(u, self.w2[li])
         return 1
 
-    def _post(self, rt, sp: int, step: torch.Tensor, T: int, n_last: int):
+    def _post(self, rt, sp: int, step: torch.Tensor, T: int, n_last: int, has_ext: bool):
         cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
         dm = cfg.model_dim
         n = self._layer_tail(rt, 0, T)
         for li in range(1, cfg.layers):
             n += self._layer_head(rt, li, T)
-            n += self._attn(rt, sp, li, T)
+            n += self._attn(rt, sp, li, T, has_ext)
             n += self._layer_tail(rt, li, T)
         off = L.HEADER_INTS                     # `last` is packed first (stepdesc.pack)
         idx = step[off: off + n_last].long()
@@ -532,17 +542,19 @@ class B200Transformer:
 
     def forward_rows(self, rt: StepRuntime, step: torch.Tensor, sd: StepDesc):
         """The batched forward over staged rows (model.py:137-164 for every segment).
-        Graph mode replays the captured graphs of the step's row bucket."""
+        Graph mode replays the captured graphs of (row bucket, has multi-token rows)."""
         timed = rt.attn_events
         ev = [] if timed is not None else None
+        has_ext = bool(sd.ext)
         if rt.graph_bucket(sd.n_rows) is not None and sd.rows_pad:
             Tb = sd.rows_pad
             if step.data_ptr() != rt.gstep.data_ptr():
                 rt.gstep[: step.numel()].copy_(step)
-            g = rt.graphs.get(Tb)
+            key = (Tb, has_ext)
+            g = rt.graphs.get(key)
             if g is None:
-                g = self._capture(rt, Tb, sd.last_pad)
-                rt.graphs[Tb] = g
+                g = self._capture(rt, Tb, sd.last_pad, has_ext)
+                rt.graphs[key] = g
             pe = rt.phase_events
             if pe is not None:
                 evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -550,21 +562,21 @@ class B200Transformer:
             g["pre"].replay()
             if pe is not None:
                 evs[1].record()
-            n_att = self._attn(rt, rt.gstep.data_ptr(), 0, Tb, ev)
+            n_att = self._attn(rt, rt.gstep.data_ptr(), 0, Tb, has_ext, ev)
             if pe is not None:
                 evs[2].record()
             g["post"].replay()
             if pe is not None:
                 evs[3].record()
-                pe.append((Tb, len(sd.dec), sum(sg[1] + sg[2] for sg in sd.segs), evs))
+                pe.append((key, len(sd.dec), sum(sg[1] + sg[2] for sg in sd.segs), evs))
             rt.launches += g["launches"] + n_att
             logits, toks = g["logits"][: len(sd.last)].clone(), g["toks"]
         else:
             T = sd.n_rows
             sp = step.data_ptr()
             n = self._pre(rt, sp, T)
-            n += self._attn(rt, sp, 0, T, ev)
-            m, logits, toks = self._post(rt, sp, step, T, len(sd.last))
+            n += self._attn(rt, sp, 0, T, has_ext, ev)
+            m, logits, toks = self._post(rt, sp, step, T, len(sd.last), has_ext)
             rt.launches += n + m
         if ev:
             timed.append((ev[0][0], ev[0][1], sd))
@@ -572,7 +584,7 @@ class B200Transformer:
         rt.last_tokens = toks
         return toks
 
-    def _capture(self, rt: StepRuntime, Tb: int, n_last: int) -> dict:
+    def _capture(self, rt: StepRuntime, Tb: int, n_last: int, has_ext: bool) -> dict:
         """Capture the pre (embed + layer-0 head) and post (rest) phases for a row
         bucket; the descriptor is read from the fixed rt.gstep buffer."""
         sp = rt.gstep.data_ptr()
@@ -580,14 +592,14 @@ class B200Transformer:
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):          # warm-up (cuBLAS handles, heuristics)
             self._pre(rt, sp, Tb)
-            self._attn(rt, sp, 0, Tb)
-            self._post(rt, sp, rt.gstep, Tb, n_last)
+            self._attn(rt, sp, 0, Tb, has_ext)
+            self._post(rt, sp, rt.gstep, Tb, n_last, has_ext)
         torch.cuda.current_stream().wait_stream(side)
         pre, post = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(pre):
             n_pre = self._pre(rt, sp, Tb)
         with torch.cuda.graph(post):
-            n_post, logits, toks = self._post(rt, sp, rt.gstep, Tb, n_last)
+            n_post, logits, toks = self._post(rt, sp, rt.gstep, Tb, n_last, has_ext)
         return {"pre": pre, "post": post, "logits": logits, "toks": toks,
                 "launches": n_pre + n_post}
 

@@ -13,7 +13,7 @@ from . import _lib as L
 _HDR = [
     "n_rows", "n_rows_pad", "n_new", "n_segs", "n_dec", "n_ext", "n_jobs", "n_ops", "n_phases",
     "n_last", "dec_total", "off_new", "off_segs", "off_dec", "off_dec_prefix", "off_ext", "off_jobs",
-    "off_spans", "off_ops", "off_phases", "off_last",
+    "off_spans", "off_ops", "off_phases", "off_last", "ext_total", "off_ext_prefix",
 ]
 
 
@@ -26,8 +26,8 @@ class StepDesc:
     def __init__(self):
         self.new: list = []      # (slot, logical_idx, token, row, live_idx)
         self.segs: list = []     # (slot, m, n, row_off)
-        self.dec: list = []      # (row, slot, kv_len)
-        self.ext: list = []      # (row_off, slot, m, n, q0)
+        self.dec: list = []      # decode tiles (row, slot, kv_len, nq, m, group)
+        self.ext: list = []      # multi-token tiles (row, slot, kv_len, nq, m, group)
         self.jobs: list = []     # (slot, old_len, s, reencode_from, span_off, n_spans, out_row, keep)
         self.spans: list = []    # start, end (flattened pairs)
         self.ops: list = []      # (kind, slot, table_off, count, sp_before, owner)
@@ -85,6 +85,13 @@ class StepDesc:
         parts.append(prefix.astype(np.int32))
         off += prefix.size
         add("ext", self.ext, L.EXT_FIELDS)
+        eprefix = np.zeros(len(self.ext) + 1, dtype=np.int64)
+        if self.ext:
+            eprefix[1:] = np.cumsum([e[2] for e in self.ext])
+        assert eprefix[-1] < 2**31
+        hdr["off_ext_prefix"] = off
+        parts.append(eprefix.astype(np.int32))
+        off += eprefix.size
         add("jobs", self.jobs, L.JOB_FIELDS)
         add("spans", self.spans, 0)
         add("ops", self.ops, L.OP_FIELDS)
@@ -97,7 +104,7 @@ class StepDesc:
             n_rows_pad=self.n_rows if self.rows_pad is None else max(self.rows_pad, self.n_rows),
             n_new=len(self.new), n_segs=len(self.segs), n_dec=len(self.dec), n_ext=len(self.ext),
             n_jobs=len(self.jobs), n_ops=len(self.ops), n_phases=len(self.phase_starts),
-            n_last=len(last), dec_total=int(prefix[-1]),
+            n_last=len(last), dec_total=int(prefix[-1]), ext_total=int(eprefix[-1]),
         )
         self.offsets = hdr
         head = np.zeros(L.HEADER_INTS, dtype=np.int32)

@@ -65,16 +65,16 @@ def test_decode_bf16_matches_oracle(n_ctas, hq, hkv):
     q = torch.randn(len(lengths), hq, d, device="cuda", generator=g).to(torch.bfloat16)
     sd = StepDesc()
     for i, n in enumerate(lengths):
-        sd.dec.append((i, i, n, 1, n - 1))
+        sd.dec.append((i, i, n, 1, n - 1, 0))
     step = _dev(sd.pack())
     out = torch.zeros(len(lengths), hq, d, device="cuda", dtype=torch.bfloat16)
     sms = L.load().tim_sm_count()
     ctas = sms if n_ctas is None else n_ctas
     ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, len(lengths), hkv, d), device="cuda")
-    cnt = torch.zeros(len(lengths) * hkv, device="cuda", dtype=torch.int32)
+    cnt = torch.zeros(len(lengths) * 8, device="cuda", dtype=torch.int32)
     tab_d = _dev(tab)
     for _ in range(2):  # twice: counters must self-reset
-        L.call("tim_attn_decode", _ptr(step), _ptr(q), _ptr(out), _ptr(kp), _ptr(vp), _ptr(tab_d),
+        L.call("tim_attn_decode", _ptr(step), 0, _ptr(q), _ptr(out), _ptr(kp), _ptr(vp), _ptr(tab_d),
                stride, hq, hkv, d, 1.0 / np.sqrt(d), _ptr(ws), _ptr(cnt), ctas, len(lengths),
                L.DTYPE_BF16, _stream())
         torch.cuda.synchronize()
@@ -116,22 +116,28 @@ def test_extend_tiles_bf16_matches_oracle(hq, hkv, n_ctas):
     segs = [(0, 1), (0, 7), (5, 33), (100, 64), (700, 150), (0, 200), (1200, 3), (40, 1)]
     kp, vp, tab, stride, q, sd, rows = _extend_case(hq, hkv, d, torch.bfloat16, segs, 11)
     qpi = L.load().tim_extend_queries_per_item(hq, hkv, d, L.DTYPE_BF16)
-    assert qpi == 16 // (hq // hkv)
+    ngr = L.load().tim_extend_head_groups(hkv)
+    assert qpi * (hq // hkv) == 16 * (8 * ngr // hkv)
     row = 0
     for i, (m, n) in enumerate(segs):
-        for q0 in range(0, n, qpi):
+        if n == 1:
+            sd.dec.append((row, i, m + 1, 1, m, 0))
+        for q0 in range(0, n if n > 1 else 0, qpi):
             nq = min(qpi, n - q0)
-            sd.dec.append((row + q0, i, m + q0 + nq, nq, m))
+            for gi in range(ngr):
+                sd.ext.append((row + q0, i, m + q0 + nq, nq, m, gi))
         row += n
     step = _dev(sd.pack())
     out = torch.zeros(rows, hq, d, device="cuda", dtype=torch.bfloat16)
     ctas = n_ctas or L.load().tim_sm_count()
-    ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, len(sd.dec), hkv, d), device="cuda")
-    cnt = torch.zeros(len(sd.dec) * hkv, device="cuda", dtype=torch.int32)
+    ntiles = len(sd.dec) + len(sd.ext)
+    ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, ntiles, hkv, d), device="cuda")
+    cnt = torch.zeros(ntiles * 8, device="cuda", dtype=torch.int32)
     tab_d = _dev(tab)
-    L.call("tim_attn_decode", _ptr(step), _ptr(q), _ptr(out), _ptr(kp), _ptr(vp), _ptr(tab_d),
-           stride, hq, hkv, d, 1.0 / np.sqrt(d), _ptr(ws), _ptr(cnt), ctas, len(sd.dec),
-           L.DTYPE_BF16, _stream())
+    for mode in (0, 1):
+        L.call("tim_attn_decode", _ptr(step), mode, _ptr(q), _ptr(out), _ptr(kp), _ptr(vp),
+               _ptr(tab_d), stride, hq, hkv, d, 1.0 / np.sqrt(d), _ptr(ws), _ptr(cnt), ctas,
+               ntiles, L.DTYPE_BF16, _stream())
     torch.cuda.synchronize()
     assert int(cnt.abs().sum()) == 0
     kf, vf, qf = kp.float().cpu().numpy(), vp.float().cpu().numpy(), q.float().cpu().numpy()

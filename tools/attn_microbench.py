@@ -44,17 +44,17 @@ def main():
     tab_d = torch.from_numpy(tab).cuda()
     sd = StepDesc()
     for i, n in enumerate(lens):
-        sd.dec.append((i, i, int(n), 1, int(n) - 1))
+        sd.dec.append((i, i, int(n), 1, int(n) - 1, 0))
     step = torch.from_numpy(sd.pack()).cuda()
     q = torch.randn(a.batch, hq, d, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)
     ctas = a.ctas or L.load().tim_sm_count()
     ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, a.batch, hkv, d), device="cuda")
-    cnt = torch.zeros(a.batch * hkv, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(a.batch * 8, dtype=torch.int32, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
 
     def run(l):
-        L.call("tim_attn_decode", step.data_ptr(), q.data_ptr(), out.data_ptr(), K[l].data_ptr(),
+        L.call("tim_attn_decode", step.data_ptr(), 0, q.data_ptr(), out.data_ptr(), K[l].data_ptr(),
                V[l].data_ptr(), tab_d.data_ptr(), stride, hq, hkv, d, 1 / np.sqrt(d), ws.data_ptr(),
                cnt.data_ptr(), ctas, a.batch, L.DTYPE_BF16, st)
 

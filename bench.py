@@ -117,13 +117,13 @@ def reduce_over_ranks(dist, times, counts, device="cpu"):
 
 
 # --------------------------------------------------------------------- GPU arm
-def build_engine(rank: int, n_req: int, threshold: int):
+def build_engine(rank: int, n_req: int, threshold: int, pool_per_req: int = 1600):
     import paper_2507_16784_b200 as tr
     from paper_2507_16784_b200.traces import make_trace_from_text
     cfg = tr.qwen3_8b_shape()
     model = tr.B200Transformer(cfg)
     traces = [make_trace_from_text(d) for d in workload_docs(rank, n_req)]
-    pool_pages = n_req * 1600
+    pool_pages = n_req * pool_per_req
     eng = tr.Engine(model, tr.BatchConfig(max_batch=n_req, buffer_threshold=threshold,
                                           position_limit=cfg.position_limit, pool_pages=pool_pages,
                                           max_queue=max(64, n_req), check_masks=False,
@@ -135,104 +135,116 @@ def build_engine(rank: int, n_req: int, threshold: int):
 
 
 def run_gpu(args, rank: int, world: int, dist):
+    """value and e2e over the SAME K steps of the trajectories: engine A plans
+    them on the host and replays them from device-resident descriptors (value,
+    GPU-only); engine B — a fresh engine on the same traces, advanced to the
+    same step — runs them through the public Engine.step() (e2e: host planning,
+    pinned H2D of each step's descriptor, D2H of each step's greedy tokens)."""
     import torch
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-    eng, cfg, model = build_engine(rank, args.batch, args.threshold)
-    rt = eng.runtime
-    kv_tok_layer = cfg.n_kv * cfg.head_dim * 2 * 2          # K+V bytes per token per layer (bf16)
-    q_o_bytes = cfg.heads * cfg.head_dim * 2 * 2            # q in + ctx out per decode query
+    cfg = None
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    def steps(n):
+    def steps(eng, n):
         tok = 0
         for _ in range(n):
             rep = eng.step()
             tok += sum(rep.decoded.values())
         return tok
 
-    t0 = time.perf_counter()
-    rt.precapture()
-    print(f"[rank {rank}] captured {len(rt.graphs)} step graphs in {time.perf_counter() - t0:.1f} s",
-          file=sys.stderr)
-    steps(args.skip)
-    steps(args.warmup)
-    barrier()
+    def prepare():
+        eng, cfg_, model = build_engine(rank, args.batch, args.threshold)
+        t0 = time.perf_counter()
+        eng.runtime.precapture()
+        print(f"[rank {rank}] captured {len(eng.runtime.graphs)} step graphs in "
+              f"{time.perf_counter() - t0:.1f} s", file=sys.stderr)
+        steps(eng, args.skip)
+        steps(eng, args.warmup)
+        barrier()
+        return eng, cfg_, model
 
-    # The timed region alternates blocks of `--block` steps: a value block
-    # (steps planned on the host first, then replayed from device-resident
-    # descriptors: GPU-only time) and an e2e block (the next steps through the
-    # public Engine.step(): host planning + pinned H2D of the descriptor + D2H
-    # of the step's greedy tokens).  Both arms thus sample the same phase of
-    # the trajectories; each times exactly `--steps` steps.
+    # ---------------------------------------------------------------- value
+    eng, cfg, model = prepare()
+    rt = eng.runtime
+    kv_tok_layer = cfg.n_kv * cfg.head_dim * 2 * 2          # K+V bytes per token per layer (bf16)
+    q_o_bytes = cfg.heads * cfg.head_dim * 2 * 2            # q in + ctx out per decode query
     attn_store = []
     phase_store = [] if os.environ.get("TIMRUN_PHASES") else None
+    rt.recording = []
+    planned_tokens = steps(eng, args.steps)
+    records, rt.recording = rt.recording, None
+    resident = rt.replay_upload(records)
+    rows = sorted(sd.n_rows for sd, _, _ in records)
+    launches0 = rt.launches
+    rt.attn_events, rt.phase_events = attn_store, phase_store
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
-    host_bufs = [torch.empty(args.batch * 2, dtype=torch.int32, pin_memory=True) for _ in range(2)]
-    result_sum = e2e_steps = 0
-    ms = e2e_ms = wall_ms = 0.0
-    planned_tokens = e2e_tokens = 0
-    launches = h2d = d2h = 0
-    rows = []
     clocks.start()
-    done = 0
-    while done < args.steps:
-        nb = min(args.block, args.steps - done)
-        rt.recording = []
-        planned_tokens += steps(nb)
-        records, rt.recording = rt.recording, None
-        resident = rt.replay_upload(records)
-        rows += [sd.n_rows for sd, _, _ in records]
-        launches0 = rt.launches
-        rt.attn_events, rt.phase_events = attn_store, phase_store
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        rt.replay(resident)
-        e1.record()
-        barrier()
-        ms += e0.elapsed_time(e1)
-        launches += rt.launches - launches0
-        rt.attn_events = rt.phase_events = None
-        w0 = time.perf_counter()
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        f0.record()
-        pend = None
-        for _ in range(nb):
-            rep = eng.step()
-            e2e_tokens += sum(rep.decoded.values())
-            h2d += rt._last_upload_bytes
-            toks = eng.last_step_tokens
-            if pend is not None:                   # read step k-1's result while step k runs
-                ev, buf, n = pend
-                ev.synchronize()
-                result_sum += int(buf[:n].sum())
-                pend = None
-            if toks is not None:
-                n = toks.numel()
-                buf = host_bufs[len(host_bufs) - 1 - (e2e_steps % 2)]
-                buf[:n].copy_(toks, non_blocking=True)   # D2H of the step's greedy tokens
-                ev = torch.cuda.Event()
-                ev.record()
-                pend = (ev, buf, n)
-                d2h += n * 4
-            e2e_steps += 1
-        if pend is not None:
-            pend[0].synchronize()
-            result_sum += int(pend[1][:pend[2]].sum())
-        f1.record()
-        barrier()
-        e2e_ms += f0.elapsed_time(f1)
-        wall_ms += (time.perf_counter() - w0) * 1000.0
-        done += nb
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rt.replay(resident)
+    e1.record()
+    barrier()
     clk = clocks.stop()
-    rows.sort()
-    print(f"[rank {rank}] rows/step in the value blocks: min {rows[0]} median {rows[len(rows) // 2]} "
+    ms = e0.elapsed_time(e1)
+    launches = rt.launches - launches0
+    rt.attn_events = rt.phase_events = None
+    weight_gb = model.weight_bytes() / 1e9
+    del eng, rt, model, resident, records
+    torch.cuda.empty_cache()
+
+    # ------------------------------------------------------------------ e2e
+    eng, _, model = prepare()
+    rt = eng.runtime
+    host_bufs = [torch.empty(args.batch * 2, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+    result_sum = 0
+    host_step_ms = []
+    h2d = d2h = 0
+    e2e_tokens = 0
+    barrier()
+    w0 = time.perf_counter()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record()
+    pend = None
+    for k in range(args.steps):
+        th = time.perf_counter()
+        rep = eng.step()
+        host_step_ms.append((time.perf_counter() - th) * 1000.0)
+        e2e_tokens += sum(rep.decoded.values())
+        h2d += rt._last_upload_bytes
+        toks = eng.last_step_tokens
+        if pend is not None:                       # read step k-1's result while step k runs
+            ev, buf, n = pend
+            ev.synchronize()
+            result_sum += int(buf[:n].sum())
+            pend = None
+        if toks is not None:
+            n = toks.numel()
+            buf = host_bufs[k % 2]
+            buf[:n].copy_(toks, non_blocking=True)   # D2H of the step's greedy tokens
+            ev = torch.cuda.Event()
+            ev.record()
+            pend = (ev, buf, n)
+            d2h += n * 4
+    if pend is not None:
+        pend[0].synchronize()
+        result_sum += int(pend[1][:pend[2]].sum())
+    f1.record()
+    barrier()
+    e2e_ms = f0.elapsed_time(f1)
+    wall_ms = (time.perf_counter() - w0) * 1000.0
+    assert e2e_tokens == planned_tokens, (e2e_tokens, planned_tokens)
+    hs = sorted(host_step_ms)
+    print(f"[rank {rank}] e2e host time inside Engine.step(): mean {sum(hs) / len(hs):.2f} ms, "
+          f"median {hs[len(hs) // 2]:.2f}, p90 {hs[int(len(hs) * 0.9)]:.2f}, max {hs[-1]:.2f}",
+          file=sys.stderr)
+    print(f"[rank {rank}] rows/step in the timed steps: min {rows[0]} median {rows[len(rows) // 2]} "
           f"p90 {rows[int(len(rows) * 0.9)]} max {rows[-1]} mean {sum(rows) / len(rows):.0f}",
           file=sys.stderr)
     if phase_store:
@@ -262,14 +274,14 @@ def run_gpu(args, rank: int, world: int, dist):
 
     print(f"[rank {rank}] value window: {planned_tokens} tokens in {ms:.1f} ms; e2e window: "
           f"{e2e_tokens} tokens in {e2e_ms:.1f} ms GPU / {wall_ms:.1f} ms wall; "
-          f"graphs={len(rt.graphs)} launches={launches}", file=sys.stderr)
+          f"launches={launches}", file=sys.stderr)
     ms, e2e_ms, planned_tokens, e2e_tokens = reduce_over_ranks(
         dist, [ms, e2e_ms], [planned_tokens, e2e_tokens], device="cuda")
     return dict(ms=ms, e2e_ms=e2e_ms, wall_ms=wall_ms, tokens=planned_tokens, e2e_tokens=e2e_tokens,
                 attn_ms=attn_ms, attn_bytes=attn_bytes, launches=launches, clocks=clk,
                 dec_ms=dec_ms, dec_bytes=dec_bytes, n_dec_launches=len(dec_only), n_attn=len(attn),
                 h2d=h2d / args.steps, d2h=d2h / args.steps, mean_live=mean_live,
-                weight_gb=model.weight_bytes() / 1e9)
+                weight_gb=weight_gb)
 
 
 # --------------------------------------------------------------- CPU reference
@@ -378,7 +390,6 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--skip", type=int, default=1500)
-    ap.add_argument("--block", type=int, default=20)
     ap.add_argument("--batch", type=int, default=PER_GPU)
     ap.add_argument("--threshold", type=int, default=2)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
   uint64_t* empty = full + C::STAGES;
   int* sflag = reinterpret_cast<int*>(empty + C::STAGES);
 
+  griddep_launch();   // let the next kernel (o_proj GEMM) start prefetching its weights
   unsigned long long* trace = g_trace;
   if (trace && threadIdx.x == 0) trace[4 * blockIdx.x] = gtimer();
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
@@ -261,12 +262,16 @@ __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
         l_r[h] = l_r[h] * corr[h] + sum;
         m_r[h] = mnew;
       }
+      // Rescale O only when some row's running max moved (warp-uniform test):
+      // after the first tiles of a query this is rare, and it is 64 FMULs.
+      if (__any_sync(0xffffffffu, corr[0] != 1.f || corr[1] != 1.f)) {
 #pragma unroll
-      for (int i = 0; i < C::NT; ++i) {
-        o[i][0] *= corr[0];
-        o[i][1] *= corr[0];
-        o[i][2] *= corr[1];
-        o[i][3] *= corr[1];
+        for (int i = 0; i < C::NT; ++i) {
+          o[i][0] *= corr[0];
+          o[i][1] *= corr[0];
+          o[i][2] *= corr[1];
+          o[i][3] *= corr[1];
+        }
       }
       const uint32_t pa0 = pack_bf16(v[0][0], v[0][1]);
       const uint32_t pa1 = pack_bf16(v[1][0], v[1][1]);

@@ -109,6 +109,7 @@ template <typename T>
 __global__ void __launch_bounds__(128)
     silu_rms_kernel(T* __restrict__ u, int width, const T* __restrict__ h, int dm, float eps) {
   constexpr int V = Vec<T>::V;
+  griddep_launch();   // the down-projection GEMM may start streaming its weights
   const int r = blockIdx.x;
   const float inv = h ? row_inv_rms(h + (int64_t)r * dm, dm, eps) : 1.f;
   const int nv = width / V;

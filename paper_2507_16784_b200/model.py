@@ -20,6 +20,7 @@ per-row kernels are libtimrun.
 
 from __future__ import annotations
 
+import ctypes
 import json
 import math
 import os
@@ -168,6 +169,7 @@ class StepRuntime:
         self.graph_pool = None
         self.gstep = None
         self.recording = None        # list -> record descriptors instead of executing
+        self.prologue_events = None  # list -> CUDA events around K4 + K5 + staging
         self.phase_events = None     # list -> CUDA events around pre / attn0 / post (diagnostics)
         self.attn_events = None      # list -> CUDA events around layer-0 decode attention
 
@@ -276,6 +278,10 @@ class StepRuntime:
     def _execute(self, sd: StepDesc, step: torch.Tensor, forward: bool):
         st = stream_handle()
         tstride = self.tables.shape[1]
+        pev = self.prologue_events
+        if pev is not None:
+            p0 = torch.cuda.Event(enable_timing=True)
+            p0.record()
         if sd.jobs:
             L.call("tim_prune_compact", step.data_ptr(), len(sd.jobs), self.live.data_ptr(),
                    self.live.shape[1], self.logical.data_ptr(), self.logical.shape[1],
@@ -290,6 +296,10 @@ class StepRuntime:
                    self.logical.shape[1], self.row_tokens.data_ptr(), self.row_pages.data_ptr(),
                    self.row_pos.data_ptr(), st)
             self.launches += 2
+        if pev is not None:
+            p1 = torch.cuda.Event(enable_timing=True)
+            p1.record()
+            pev.append((p0, p1, sd))
         if not forward or sd.n_rows == 0 or self.model is None or not self.model.has_weights:
             return None
         return self.model.forward_rows(self, step, sd)
@@ -330,15 +340,19 @@ class B200Transformer:
         if cfg.precision == "float32":
             torch.backends.cuda.matmul.allow_tf32 = False
             torch.backends.cudnn.allow_tf32 = False
+        # Projection weights are stored transposed ([out, in], K contiguous): an
+        # output-column block is then one contiguous slab for the decode GEMM's
+        # TMA weight stream; `wqkv[li]` etc. remain the reference's [in, out].
         if cfg.weight_init == "reference":
             emb, layers = _reference_weights(cfg)
             self.emb = torch.from_numpy(emb).to(self.dev, dt)
-            self.wqkv, self.wo, self.w1, self.w2 = [], [], [], []
+            self.wqkv_t, self.wo_t, self.w1_t, self.w2_t = [], [], [], []
             for wq, wk, wv, wo, w1, w2 in layers:
-                self.wqkv.append(torch.from_numpy(np.concatenate([wq, wk, wv], axis=1)).to(self.dev, dt))
-                self.wo.append(torch.from_numpy(wo).to(self.dev, dt))
-                self.w1.append(torch.from_numpy(w1).to(self.dev, dt))
-                self.w2.append(torch.from_numpy(w2).to(self.dev, dt))
+                qkv = np.concatenate([wq, wk, wv], axis=1)
+                self.wqkv_t.append(torch.from_numpy(np.ascontiguousarray(qkv.T)).to(self.dev, dt))
+                self.wo_t.append(torch.from_numpy(np.ascontiguousarray(wo.T)).to(self.dev, dt))
+                self.w1_t.append(torch.from_numpy(np.ascontiguousarray(w1.T)).to(self.dev, dt))
+                self.w2_t.append(torch.from_numpy(np.ascontiguousarray(w2.T)).to(self.dev, dt))
         else:
             g = torch.Generator(device=self.dev).manual_seed(cfg.seed)
             sc = 1.0 / math.sqrt(dm)
@@ -348,10 +362,22 @@ class B200Transformer:
 
             self.emb = mat(cfg.vocab, dm)
             W = (hq + 2 * hkv) * D
-            self.wqkv = [mat(dm, W) for _ in range(cfg.layers)]
-            self.wo = [mat(dm, dm) for _ in range(cfg.layers)]
-            self.w1 = [mat(dm, cfg.n_mlp) for _ in range(cfg.layers)]
-            self.w2 = [mat(cfg.n_mlp, dm) for _ in range(cfg.layers)]
+            self.wqkv_t = [mat(W, dm) for _ in range(cfg.layers)]
+            self.wo_t = [mat(dm, dm) for _ in range(cfg.layers)]
+            self.w1_t = [mat(cfg.n_mlp, dm) for _ in range(cfg.layers)]
+            self.w2_t = [mat(dm, cfg.n_mlp) for _ in range(cfg.layers)]
+        self.wqkv = [w.t() for w in self.wqkv_t]
+        self.wo = [w.t() for w in self.wo_t]
+        self.w1 = [w.t() for w in self.w1_t]
+        self.w2 = [w.t() for w in self.w2_t]
+        # weight-streaming decode GEMM (tim_gemm_skinny) for steps of <= 64 rows
+        W = (hq + 2 * hkv) * D
+        self.skinny = (cfg.precision == "bfloat16" and os.environ.get("TIMRUN_SKINNY", "0") == "1"
+                       and all(n % 64 == 0 for n in (W, dm, cfg.n_mlp))
+                       and all(k % 256 == 0 for k in (dm, cfg.n_mlp)))
+        if self.skinny:
+            self.tmaps = [[self._tmap(w) for w in (self.wqkv_t[li], self.wo_t[li], self.w1_t[li],
+                                                   self.w2_t[li])] for li in range(cfg.layers)]
         self.emb_t = self.emb.t().contiguous()     # tied LM head (model.py:164)
         cos, sin = _rope_tables(cfg)
         self.cos = torch.from_numpy(cos).to(self.dev)
@@ -361,6 +387,30 @@ class B200Transformer:
             hq, hkv, D, L.DTYPE_BF16) < (1 << 30))
         self.tile_q = 16 // (hq // hkv) if self.tensor_cores else 0   # queries per mode-0 tile
         self._runtimes: dict[int, StepRuntime] = {}
+
+    @staticmethod
+    def _tmap(t: torch.Tensor):
+        """128-byte TMA descriptor of a row-major bf16 matrix with 64x64 boxes."""
+        buf = (ctypes.c_uint8 * 128)()
+        L.call("tim_tmap_2d_bf16", ctypes.addressof(buf), t.data_ptr(), t.shape[0], t.shape[1], 64, 64)
+        return buf
+
+    def _gemm(self, rt, li: int, which: int, x, y, res, T: int) -> int:
+        """y (+)= x @ W for projection `which` (0 qkv, 1 o, 2 up, 3 down):
+        the weight-streaming kernel for <= 64 rows, cuBLAS otherwise."""
+        wt = (self.wqkv_t, self.wo_t, self.w1_t, self.w2_t)[which][li]
+        if self.skinny and T <= 64:
+            N, K = wt.shape
+            L.call("tim_gemm_skinny", ctypes.addressof(rt.x_maps[id(x)]),
+                   ctypes.addressof(self.tmaps[li][which]), y.data_ptr(),
+                   None if res is None else res.data_ptr(), T, N, K, rt.gws.data_ptr(),
+                   rt.gcnt.data_ptr(), rt.sms, stream_handle())
+            return 1
+        if res is None:
+            torch.matmul(x[:T], wt.t(), out=y[:T])
+        else:
+            y[:T].addmm_(x[:T], wt.t())
+        return 0
 
     # ------------------------------------------------------- protocol
     @property
@@ -379,7 +429,7 @@ class B200Transformer:
         return StepRuntime(self, pool, max_slots, logical_cap)
 
     def weight_bytes(self) -> int:
-        t = [self.emb] + self.wqkv + self.wo + self.w1 + self.w2
+        t = [self.emb] + self.wqkv_t + self.wo_t + self.w1_t + self.w2_t
         return sum(x.numel() * x.element_size() for x in t)
 
     def _protocol_runtime(self, pool: DevicePagePool) -> StepRuntime:
@@ -460,6 +510,12 @@ class B200Transformer:
         rt.max_dec = R
         rt.ws = torch.zeros(L.load().tim_decode_ws_floats(n_ctas, R, cfg.n_kv, D), device=d)
         rt.counters = torch.zeros(R * 8, dtype=torch.int32, device=d)
+        if self.skinny:   # decode-GEMM activation descriptors (buffers are fixed) + workspace
+            rt.x_maps = {id(t): self._tmap(t) for t in (rt.h, rt.ctx, rt.u)}
+            rt.gws = torch.zeros(L.load().tim_gemm_ws_floats(n_ctas, max(cfg.n_mlp, dm, 4096)),
+                                 device=d)
+            rt.gcnt = torch.zeros(max(cfg.n_mlp, dm, (cfg.heads + 2 * cfg.n_kv) * D) // 64,
+                                  dtype=torch.int32, device=d)
 
     # The forward is split in three phases so that a decode step can run as
     # two captured CUDA graphs around one eagerly launched layer-0 attention
@@ -475,12 +531,12 @@ class B200Transformer:
         """QKV GEMM on the raw residual + fused RMSNorm-scale/RoPE/page store."""
         cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
         dm, D = cfg.model_dim, cfg.head_dim
-        torch.matmul(rt.h[:T], self.wqkv[li], out=rt.qkv[:T])
+        n = self._gemm(rt, li, 0, rt.h, rt.qkv, None, T)
         L.call("tim_rope_kv_store", rt.qkv.data_ptr(), rt.h.data_ptr(), dm, 1e-6, T,
                rt.row_pos.data_ptr(), rt.row_pages.data_ptr(), self.cos.data_ptr(),
                self.sin.data_ptr(), cfg.heads, cfg.n_kv, D, rt.q.data_ptr(),
                self.pool_layer(rt.pool.K_layers, li), self.pool_layer(rt.pool.V_layers, li), td, st)
-        return 1
+        return 1 + n
 
     def _attn(self, rt, sp: int, li: int, T: int, has_ext: bool, timed=None) -> int:
         """Attention of one layer: the split-K tile kernel over the decode tiles
@@ -514,13 +570,11 @@ class B200Transformer:
         """h += ctx @ wo; u = silu(rms(h) @ w1) (scale fused); h += u @ w2."""
         cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
         dm = cfg.model_dim
-        h = rt.h[:T]
-        h.addmm_(rt.ctx[:T], self.wo[li])
-        u = rt.u[:T]
-        torch.matmul(h, self.w1[li], out=u)
-        L.call("tim_silu_rms", u.data_ptr(), T, cfg.n_mlp, rt.h.data_ptr(), dm, 1e-6, td, st)
-        h.addmm_(u, self.w2[li])
-        return 1
+        n = self._gemm(rt, li, 1, rt.ctx, rt.h, rt.h, T)
+        n += self._gemm(rt, li, 2, rt.h, rt.u, None, T)
+        L.call("tim_silu_rms", rt.u.data_ptr(), T, cfg.n_mlp, rt.h.data_ptr(), dm, 1e-6, td, st)
+        n += self._gemm(rt, li, 3, rt.u, rt.h, rt.h, T)
+        return 1 + n
 
     def _post(self, rt, sp: int, step: torch.Tensor, T: int, n_last: int, has_ext: bool):
         cfg, st, td = self.config, stream_handle(), self.config.tim_dtype

@@ -333,3 +333,81 @@ def test_apply_device_matches_reference_cases():
                                               list(range(n)), tokens)
         assert new_live == opr.surgery(list(range(n)), [opr.Span(a, b)])
         assert suffix == [tokens[i] for i in new_live[start:]]
+
+
+# ----------------------------------------------------- scheduler behaviours
+def _scripted(threshold=1, P=4096, hub=None, **kw):
+    return tr.Engine(tr.ScriptedModel(position_limit=P),
+                     tr.BatchConfig(buffer_threshold=threshold, position_limit=P, pool_pages=4 * P,
+                                    **kw), hub=hub)
+
+
+def _traces(golden, kind, n):
+    return [r for r in _load(golden, "events.json.gz") if r["gen"][0] == kind][:n]
+
+
+def test_non_blocking_tool_use(golden):
+    """Acceptance 5 shape (tests/test_acceptance.py:96-155): while one request
+    waits on a slow tool, the others keep decoding one token per step."""
+    import time as _time
+    hub = tr.ToolHub()
+    hub.register(tr.ToolSpec("slow", timeout_ms=10_000), lambda p, i: (_time.sleep(0.3), p)[1])
+    doc = '[{"thought":"ask","tool_name":"slow","parameters":{"q":"x"},"tool_result":{"q":"x"},' \
+          '"conclusion":"done"}]'
+    tool_trace = tr.make_trace_from_text(doc)
+    worker = _traces(golden, "deep_recursion_tree", 4)[2]   # deep(6,2)
+    eng = _scripted(threshold=1, P=8192, hub=hub, max_batch=4)
+    trid = eng.submit("t:", [tr.ToolSpec("slow", timeout_ms=10_000)], script=tool_trace.script)
+    workers = [eng.submit(f"w{i}:", script=worker["script"]) for i in range(3)]
+    window, moved = 0, {w: 0 for w in workers}
+    while not eng.all_terminal():
+        waiting = eng.requests[trid].status is tr.Status.AWAITING_TOOL
+        rep = eng.step()
+        if waiting:
+            window += 1
+            for w in workers:
+                moved[w] += rep.decoded.get(w, 0)
+    assert window >= 20
+    assert all(moved[w] >= 0.9 * min(window, len(worker["script"])) for w in workers)
+    res = eng.result(trid)
+    assert res["status"] == "finished" and '"tool_result":{"q":"x"}' in res["text"]
+
+
+def test_queue_and_prompt_limits(golden):
+    """tests/test_scheduler.py:148-168."""
+    rec = _traces(golden, "random_tree", 1)[0]
+    eng = _scripted(threshold=0, max_batch=1, max_queue=2)
+    eng.submit("a:", script=rec["script"])
+    eng.submit("b:", script=rec["script"])
+    with pytest.raises(tr.QueueFull):
+        eng.submit("c:", script=rec["script"])
+    with pytest.raises(tr.PromptTooLong):
+        _scripted(P=16).submit("x" * 16)
+
+
+def test_flops_arithmetic_series_without_pruning(golden):
+    """tests/test_scheduler.py:289-298: no pruning, empty prompt -> n(n+1)/2."""
+    rec = _traces(golden, "random_tree", 3)[2]
+    eng = _scripted(threshold=1 << 30)
+    eng.submit([], script=rec["stream"] if not rec["tool_names"] else rec["script"],
+               tools=[tr.ToolSpec(n) for n in rec["tool_names"]],
+               tool_responses={int(k): v for k, v in rec["tool_responses"].items()} or None)
+    total = 0
+    while not eng.all_terminal():
+        total += eng.step().flops_units
+    n = len(rec["stream"]) - 1
+    assert total == n * (n + 1) // 2
+
+
+def test_run_until_done_and_deadline(golden):
+    rec = _traces(golden, "deep_recursion_tree", 4)[2]
+    eng = _scripted(threshold=1)
+    eng.submit("p:", script=rec["script"])
+    with pytest.raises(tr.Deadline):
+        eng.run_until_done(deadline_s=0.0)
+    eng2 = _scripted(threshold=1)
+    rid = eng2.submit("p:", script=rec["script"])
+    out = dict(eng2.run_until_done())
+    assert out[rid]["status"] == "finished"
+    h = eng2.health()
+    assert h["finished"] == 1 and h["pool"]["free"] == h["pool"]["capacity"]

@@ -1,0 +1,141 @@
+"""BASELINE configs beyond the headline line (C1 tiny fp32, C4 long horizon, C5
+pruning ablation).  Prints one JSON object per config; results are copied to
+profiles/.  Usage: python tools/bench_configs.py --config c4 [--steps N]"""
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+import paper_2507_16784_b200 as tr  # noqa: E402
+from paper_2507_16784_b200 import _lib as L  # noqa: E402
+from paper_2507_16784_b200.traces import deep_recursion_doc, make_trace_from_text  # noqa: E402
+
+NO_PRUNING = 1 << 30
+
+
+def timed_window(eng, steps, block=20):
+    """Replay `steps` planned steps from device-resident descriptors (GPU time only)."""
+    rt = eng.runtime
+    ms, toks, pages_freed, jobs, kv_tok = 0.0, 0, 0, 0, 0
+    pro = []
+    done = 0
+    while done < steps:
+        nb = min(block, steps - done)
+        rt.recording = []
+        for _ in range(nb):
+            rep = eng.step()
+            toks += sum(rep.decoded.values())
+        recs, rt.recording = rt.recording, None
+        for sd, _, _ in recs:
+            pages_freed += sum(op[3] for op in sd.ops if op[0] == L.OP_FREE)
+            jobs += len(sd.jobs)
+            kv_tok += sum(sg[1] + sg[2] for sg in sd.segs)
+        res = rt.replay_upload(recs)
+        rt.prologue_events = pro
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rt.replay(res)
+        e1.record()
+        torch.cuda.synchronize()
+        rt.prologue_events = None
+        ms += e0.elapsed_time(e1)
+        done += nb
+    pro_ms = sum(a.elapsed_time(b) for a, b, _ in pro)
+    return dict(ms=ms, tokens=toks, pages_freed=pages_freed, prune_jobs=jobs, kv_tokens=kv_tok,
+                prologue_ms=pro_ms)
+
+
+def c2_like(threshold, skip, steps):
+    # pruning off keeps every token: ~7.1K pages per request at the end
+    eng, cfg, model = bench.build_engine(0, 64, threshold,
+                                         pool_per_req=7400 if threshold == NO_PRUNING else 1600)
+    eng.runtime.precapture()
+    for _ in range(skip):
+        eng.step()
+    w = timed_window(eng, steps)
+    kv_bytes = w["kv_tokens"] * cfg.kv_bytes_per_token() / steps
+    return {"threshold": threshold if threshold != NO_PRUNING else "none",
+            "tokens_per_s": w["tokens"] / (w["ms"] * 1e-3), "ms_per_step": w["ms"] / steps,
+            "attention_kv_bytes_per_step": kv_bytes,
+            "mean_retained_per_request": w["kv_tokens"] / steps / 64}
+
+
+def run_c5(a):
+    out = {"config": "C5 ablation: C2 (64 x tool_chain_tree(32), Qwen3-8B shape, bf16) pruning on (T=2) vs off",
+           "skip_steps": a.skip, "steps": a.steps}
+    import paper_2507_16784_b200.model as M  # noqa: F401
+    on = c2_like(2, a.skip, a.steps)
+    torch.cuda.empty_cache()
+    off = c2_like(NO_PRUNING, a.skip, a.steps)
+    out.update(on=on, off=off,
+               attention_bytes_ratio=on["attention_kv_bytes_per_step"] / off["attention_kv_bytes_per_step"],
+               tokens_per_s_ratio=on["tokens_per_s"] / off["tokens_per_s"])
+    return out
+
+
+def run_c4(a):
+    cfg = tr.qwen3_8b_shape(position_limit=16384)
+    model = tr.B200Transformer(cfg)
+    n = 32
+    eng = tr.Engine(model, tr.BatchConfig(max_batch=n, buffer_threshold=2, position_limit=16384,
+                                          pool_pages=n * 2048, max_queue=64, check_masks=False,
+                                          max_output_tokens=140_000))
+    for i in range(n):
+        t = make_trace_from_text(deep_recursion_doc(8, 3, seed=i, text_chars=16))
+        eng.submit(f"g{i}:", script=t.script)
+    eng.runtime.precapture()
+    t0 = time.perf_counter()
+    for _ in range(a.skip):
+        eng.step()
+    w = timed_window(eng, a.steps)
+    reqs = list(eng.requests.values())
+    return {"config": "C4 long horizon: 32 x deep_recursion(8 levels, 3-way, 16-char texts) "
+                      "= 134,480 generated tokens each, T=2, position limit 16384",
+            "skip_steps": a.skip, "steps": a.steps, "tokens_per_s": w["tokens"] / (w["ms"] * 1e-3),
+            "ms_per_step": w["ms"] / a.steps,
+            "pages_freed_per_s": w["pages_freed"] / (w["ms"] * 1e-3),
+            "prune_jobs_per_step": w["prune_jobs"] / a.steps,
+            "k4_k5_staging_us_per_step": 1000 * w["prologue_ms"] / a.steps,
+            "mean_retained_per_request": w["kv_tokens"] / a.steps / n,
+            "max_cache_so_far": max(r.metrics.max_cache for r in reqs),
+            "pruned_tokens_so_far": sum(r.metrics.pruned_tokens for r in reqs),
+            "host_s_skip": time.perf_counter() - t0}
+
+
+def run_c1(a):
+    from paper_2507_16784_b200.traces import deep_recursion_doc as _d  # noqa: F401
+    doc = deep_recursion_doc(3, 2, seed=0)
+    t = make_trace_from_text(doc)
+    cfg = tr.ModelConfig(layers=2, heads=4, head_dim=32, vocab=512, position_limit=2048)
+    eng = tr.Engine(tr.B200Transformer(cfg), tr.BatchConfig(buffer_threshold=1, position_limit=2048,
+                                                            pool_pages=4096))
+    eng.submit("p:", script=t.script)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    steps = 0
+    while not eng.all_terminal():
+        eng.step()
+        steps += 1
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    res = next(iter(eng.results.values()))
+    return {"config": "C1 tiny fp32 (2 layers, 4 heads, d_model 128), batch 1, deep(3,2), T=1",
+            "steps": steps, "wall_s": dt, "tokens_per_s": res["metrics"]["output_len"] / dt,
+            "metrics": res["metrics"]}
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", required=True, choices=["c1", "c4", "c5"])
+    ap.add_argument("--skip", type=int, default=600)
+    ap.add_argument("--steps", type=int, default=100)
+    a = ap.parse_args()
+    print(json.dumps({"c1": run_c1, "c4": run_c4, "c5": run_c5}[a.config](a)))

@@ -50,7 +50,7 @@ class FakeBackend:
         sd.segs.append((slot, m, n, row_off))
         for q0 in range(0, n, 4):
             nq = min(4, n - q0)
-            sd.dec.append((row_off + q0, slot, m + q0 + nq, nq, m))
+            sd.dec.append((row_off + q0, slot, m + q0 + nq, nq, m, 0))
 
 
 def main(steps=800):

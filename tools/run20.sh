@@ -1,0 +1,4 @@
+timeout 300 python -m pytest tests/test_gemm_gpu.py -x -q 2>&1 | tail -5
+timeout 120 python tools/gemm_custom_bench.py
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
+timeout 600 python bench.py 2>&1 | tail -2

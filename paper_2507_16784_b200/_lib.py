@@ -58,6 +58,7 @@ SIGNATURES = {
     "tim_tmap_2d_bf16": (_i32, [_p, _p, _i64, _i64, _i32, _i32]),
     "tim_gemm_ws_floats": (_i64, [_i32, _i32]),
     "tim_gemm_skinny": (_i32, [_p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _i32, _p]),
+    "tim_gemm_trace": (_i32, [_i32, _p, _i32]),
 }
 
 

@@ -373,10 +373,9 @@ class B200Transformer:
         # weight-streaming decode GEMM (tim_gemm_skinny) for steps of <= 64 rows
         W = (hq + 2 * hkv) * D
         self.skinny = (cfg.precision == "bfloat16" and os.environ.get("TIMRUN_SKINNY", "0") == "1"
-                       and all(n % 64 == 0 for n in (W, dm, cfg.n_mlp))
-                       and all(k % 256 == 0 for k in (dm, cfg.n_mlp)))
+                       and all(n % 128 == 0 for n in (W, dm, cfg.n_mlp)))
         if self.skinny:
-            self.tmaps = [[self._tmap(w) for w in (self.wqkv_t[li], self.wo_t[li], self.w1_t[li],
+            self.tmaps = [[self._tmap(w, 128) for w in (self.wqkv_t[li], self.wo_t[li], self.w1_t[li],
                                                    self.w2_t[li])] for li in range(cfg.layers)]
         self.emb_t = self.emb.t().contiguous()     # tied LM head (model.py:164)
         cos, sin = _rope_tables(cfg)
@@ -389,10 +388,11 @@ class B200Transformer:
         self._runtimes: dict[int, StepRuntime] = {}
 
     @staticmethod
-    def _tmap(t: torch.Tensor):
-        """128-byte TMA descriptor of a row-major bf16 matrix with 64x64 boxes."""
+    def _tmap(t: torch.Tensor, box_rows: int = 64):
+        """128-byte TMA descriptor of a row-major bf16 matrix, boxes of box_rows x 64."""
         buf = (ctypes.c_uint8 * 128)()
-        L.call("tim_tmap_2d_bf16", ctypes.addressof(buf), t.data_ptr(), t.shape[0], t.shape[1], 64, 64)
+        L.call("tim_tmap_2d_bf16", ctypes.addressof(buf), t.data_ptr(), t.shape[0], t.shape[1],
+               box_rows, 64)
         return buf
 
     def _gemm(self, rt, li: int, which: int, x, y, res, T: int) -> int:
@@ -512,7 +512,7 @@ class B200Transformer:
         rt.counters = torch.zeros(R * 8, dtype=torch.int32, device=d)
         if self.skinny:   # decode-GEMM activation descriptors (buffers are fixed) + workspace
             rt.x_maps = {id(t): self._tmap(t) for t in (rt.h, rt.ctx, rt.u)}
-            rt.gws = torch.zeros(L.load().tim_gemm_ws_floats(n_ctas, max(cfg.n_mlp, dm, 4096)),
+            rt.gws = torch.zeros(L.load().tim_gemm_ws_floats(n_ctas, max(cfg.n_mlp, dm, (cfg.heads + 2 * cfg.n_kv) * D)),
                                  device=d)
             rt.gcnt = torch.zeros(max(cfg.n_mlp, dm, (cfg.heads + 2 * cfg.n_kv) * D) // 64,
                                   dtype=torch.int32, device=d)

@@ -34,7 +34,7 @@ def test_skinny_gemm_matches_torch(n, k, m, ctas, residual):
     y0 = y.clone()
     ws = torch.zeros(L.load().tim_gemm_ws_floats(ctas, n), device="cuda")
     cnt = torch.zeros(n // 64, dtype=torch.int32, device="cuda")
-    tx, tw = _tmap(x), _tmap(wt)
+    tx, tw = _tmap(x), _tmap(wt, 128)
     st = torch.cuda.current_stream().cuda_stream
     for _ in range(2):   # counters self-reset
         y.copy_(y0)

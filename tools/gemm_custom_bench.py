@@ -25,7 +25,7 @@ for name, (n, k, resid) in shapes.items():
     tws = []
     for w in wts:
         b = (ctypes.c_uint8 * 128)()
-        L.call("tim_tmap_2d_bf16", ctypes.addressof(b), w.data_ptr(), n, k, 64, 64)
+        L.call("tim_tmap_2d_bf16", ctypes.addressof(b), w.data_ptr(), n, k, 128, 64)
         tws.append(b)
     st = torch.cuda.current_stream().cuda_stream
 

@@ -1,0 +1,3 @@
+timeout 300 python -m pytest tests/test_gemm_gpu.py -x -q 2>&1 | tail -3
+timeout 120 python tools/gemm_custom_bench.py
+timeout 200 python tools/gemm_trace.py > /dev/null

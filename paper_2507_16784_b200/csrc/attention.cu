@@ -14,8 +14,10 @@
 //   ring with TMA bulk copies (cp.async.bulk, SASS UBLKCP) + mbarriers, and
 //   Hkv consumer warps (one per kv head) that run QK^T and PV on the tensor
 //   cores (mma.sync m16n8k16 bf16, fp32 accumulate) with an online softmax.
-//   Queries split across CTAs are merged in-kernel (K6) by the last CTA to
-//   finish (threadfence + counter), with a log-sum-exp combine.
+//   Queries split across CTAs leave fp32 partials (fire-and-forget stores, no
+//   atomic or fence between two stages); after its stream each CTA bumps the
+//   arrival counters of its (at most two) split tiles and the last arrival
+//   merges the pieces in-kernel (K6, log-sum-exp combine).
 //   The same kernel serves extend / re-encode / prefill rows: a work item is
 //   a tile of up to 16/group consecutive queries (rows = queries x group
 //   heads of the MMA tile) with a causal limit per query.
@@ -26,8 +28,8 @@
 namespace tim {
 
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kIdChunk = 1024;      // page ids staged per producer refill (multiple of TK)
-constexpr int kFastPieces = 4;      // partials merged by the one-round-trip combine
+constexpr int kIdChunk = 512;       // page ids staged per producer refill (multiple of TK)
+constexpr int kFastPieces = 4;      // partials merged per round trip by K6
 constexpr int kMinTokensPerCta = 64;  // below this many kv tokens per CTA, use fewer CTAs
 
 // ===================================================================== K1
@@ -65,6 +67,131 @@ __device__ __forceinline__ int64_t cta_of(int64_t x, int64_t G, int64_t N) {
   return ((x + 1) * G - 1) / N;
 }
 
+// Warp-parallel search: the largest r in [0, n) with prefix[r] <= key
+// (prefix[0] = 0 <= key).  128 probes per round, all issued before any use,
+// so a list of <= 128 tiles costs one memory round trip (the serial binary
+// search it replaces cost log2(n) dependent loads at kernel start).
+TIM_DEV int seg_search(const int32_t* __restrict__ prefix, int n, int key, int lane) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int64_t span = hi - lo;
+    int32_t v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = __ldg(prefix + lo + (int)(((int64_t)(lane + 32 * j) * span) >> 7));
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cnt += __popc(__ballot_sync(0xffffffffu, v[j] <= key));
+    const int nlo = lo + (int)(((int64_t)(cnt - 1) * span) >> 7);
+    hi = cnt < 128 ? lo + (int)(((int64_t)cnt * span) >> 7) : hi;
+    lo = nlo;
+  }
+  return lo;
+}
+
+// Tile records of up to 32 consecutive tiles, lane j holding tile rb + j
+// (one round trip for the whole batch; fields fetched with shuffles).
+struct TileLane {
+  int lo, hi, qrow, slot, kv_len, nq, fresh, hgrp;
+  TIM_DEV void load(const int32_t* __restrict__ prefix, const int32_t* __restrict__ dec, int n,
+                    int rb, int lane) {
+    const int r = rb + lane;
+    if (r < n) {
+      const int32_t* rec = dec + (int64_t)r * TIM_DEC_FIELDS;
+      lo = __ldg(prefix + r);
+      hi = __ldg(prefix + r + 1);
+      qrow = __ldg(rec + 0);
+      slot = __ldg(rec + 1);
+      kv_len = __ldg(rec + 2);
+      nq = __ldg(rec + 3);
+      fresh = __ldg(rec + 4);
+      hgrp = __ldg(rec + 5);
+    } else {
+      lo = hi = 0x7fffffff;
+      qrow = slot = kv_len = nq = fresh = hgrp = 0;
+    }
+  }
+};
+#define TIM_SHFL(v, i) __shfl_sync(0xffffffffu, (v), (i))
+
+TIM_DEV int atom_add_acq_rel(int32_t* p) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
+// K6: merge of the pieces of one (tile, consumer warp) split across CTAs:
+// out = sum_p exp2(m_p - M) O_p / sum_p exp2(m_p - M) l_p.  Rows are merged 4
+// at a time and partials kFastPieces at a time with an online (running-max)
+// merge; every load of a chunk is issued before any use.
+template <int D, int HKV, int HG, int WPH>
+TIM_DEV void merge_pieces(const float* __restrict__ ws_o, const float* __restrict__ ws_ml,
+                          __nv_bfloat16* __restrict__ out, int r, int warp, int c_first, int c_last,
+                          int qrow, int nq, int hgrp, int hq, int lane) {
+  const int grp = hq / HKV, qpw = 16 / grp;
+  const int hloc = warp / WPH, sub = warp % WPH;
+  const int kvh = hgrp * HG + hloc;
+  int nw_q = nq - sub * qpw;
+  nw_q = nw_q < 0 ? 0 : (nw_q > qpw ? qpw : nw_q);
+  const int nrows = nw_q * grp;
+  for (int r0w = 0; r0w < nrows; r0w += 4) {
+    float M[4], den[4];
+    float4 acc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      M[k] = -INFINITY;
+      den[k] = 0.f;
+      acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int cb = c_first; cb <= c_last; cb += kFastPieces) {
+      float2 ml[4][kFastPieces];
+      float4 ov[4][kFastPieces];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int p = 0; p < kFastPieces; ++p) {
+          ml[k][p] = make_float2(-INFINITY, 0.f);
+          ov[k][p] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (r0w + k < nrows && cb + p <= c_last) {
+            const int64_t pr = ((int64_t)(cb + p + r) * 8 + warp) * 16 + r0w + k;
+            ml[k][p] = __ldcg(reinterpret_cast<const float2*>(ws_ml + pr * 2));
+            if (lane * 4 < D) ov[k][p] = __ldcg(reinterpret_cast<const float4*>(ws_o + pr * D) + lane);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float mc = M[k];
+#pragma unroll
+        for (int p = 0; p < kFastPieces; ++p) mc = fmaxf(mc, ml[k][p].x);
+        const float sc = M[k] == -INFINITY ? 0.f : fast_exp2(M[k] - mc);
+        den[k] *= sc;
+        acc[k].x *= sc; acc[k].y *= sc; acc[k].z *= sc; acc[k].w *= sc;
+#pragma unroll
+        for (int p = 0; p < kFastPieces; ++p) {
+          const float w = ml[k][p].x == -INFINITY ? 0.f : fast_exp2(ml[k][p].x - mc);
+          den[k] += w * ml[k][p].y;
+          acc[k].x += w * ov[k][p].x; acc[k].y += w * ov[k][p].y;
+          acc[k].z += w * ov[k][p].z; acc[k].w += w * ov[k][p].w;
+        }
+        M[k] = mc;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int rr = r0w + k;
+      if (rr < nrows && lane * 4 < D) {
+        const int qi = sub * qpw + rr / grp;
+        const int64_t oidx = (int64_t)(qrow + qi) * hq + kvh * grp + (rr % grp);
+        const float inv = 1.f / den[k];
+        uint2 pk;
+        pk.x = pack_bf16(acc[k].x * inv, acc[k].y * inv);
+        pk.y = pack_bf16(acc[k].z * inv, acc[k].w * inv);
+        *reinterpret_cast<uint2*>(out + oidx * D + lane * 4) = pk;
+      }
+    }
+  }
+}
+
 template <int D, int HKV, int HG, int WPH>
 __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
     attn_tiles_kernel(const int32_t* __restrict__ step, int list, const __nv_bfloat16* __restrict__ q,
@@ -77,85 +204,110 @@ __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
-  int* sflag = reinterpret_cast<int*>(empty + C::STAGES);
+  int32_t* s_ids = reinterpret_cast<int32_t*>(empty + C::STAGES);
 
   griddep_launch();   // let the next kernel (o_proj GEMM) start prefetching its weights
   unsigned long long* trace = g_trace;
   if (trace && threadIdx.x == 0) trace[4 * blockIdx.x] = gtimer();
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
   const int n_dec = list ? hd.n_ext : hd.n_dec;
-  const int64_t N = list ? hd.ext_total : hd.dec_total;
+  const int N = list ? hd.ext_total : hd.dec_total;
   if (n_dec == 0 || N == 0) return;
-  const int64_t want = (N + kMinTokensPerCta - 1) / kMinTokensPerCta;
-  const int64_t G = gridDim.x < want ? gridDim.x : want;
+  const int want = (N + kMinTokensPerCta - 1) / kMinTokensPerCta;
+  const int G = (int)gridDim.x < want ? (int)gridDim.x : want;
   const int c = blockIdx.x;
   if (c >= G) return;
   const int32_t* dec = step + (list ? hd.off_ext : hd.off_dec);
   const int32_t* prefix = step + (list ? hd.off_ext_prefix : hd.off_dec_prefix);
-  const int64_t start = (int64_t)c * N / G, end = (int64_t)(c + 1) * N / G;
-
-  // first segment of this CTA: largest r with prefix[r] <= start
-  int r0 = 0;
-  {
-    int lo = 0, hi = n_dec - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (prefix[mid] <= start) lo = mid; else hi = mid - 1;
-    }
-    r0 = lo;
-  }
+  const int start = (int)((int64_t)c * N / G), end = (int)((int64_t)(c + 1) * N / G);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NW);
+    for (int s2 = 0; s2 < C::STAGES; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], NW);
     }
     fence_mbar_init();
   }
+  const int r0 = seg_search(prefix, n_dec, start, lane);   // first tile of this CTA
+  TileLane tl;
+  tl.load(prefix, dec, n_dec, r0, lane);
   __syncthreads();
 
   if (warp == NW) {
     // ------------------------------------------------------------ producer
-    // Page ids of the piece are staged into shared memory a chunk at a time
-    // (one coalesced read per kIdChunk tokens), so the id latency is off the
-    // per-stage critical path; each stage is then 2*TK bulk copies.
-    int32_t* s_ids = reinterpret_cast<int32_t*>(sflag + 4);
-    int it = 0;
+    // The range is walked as chunks of <= kIdChunk tokens of one tile.  The
+    // page ids of chunk k+1 are loaded into registers while chunk k streams,
+    // so neither a chunk nor a tile switch puts an id round trip between
+    // two stages; each stage is then 2*TK bulk copies of whole page rows.
+    constexpr int IPL = kIdChunk / 32;     // ids per lane
+    int32_t idr[IPL];
+    int it = 0, rb = r0;
     bool waited = false;
-    for (int r = r0; r < n_dec && prefix[r] < end; ++r) {
-      const int64_t lo = prefix[r], hi = prefix[r + 1];
-      const int p0 = (int)((start > lo ? start : lo) - lo);
-      const int p1 = (int)((end < hi ? end : hi) - lo);
-      const int32_t* trow = tables + (int64_t)dec[r * TIM_DEC_FIELDS + 1] * tstride;
-      const int fresh = dec[r * TIM_DEC_FIELDS + 4];
-      const int64_t hoff = (int64_t)dec[r * TIM_DEC_FIELDS + 5] * HG * D;   // head-group slice
-      for (int c0 = p0; c0 < p1; c0 += kIdChunk) {
-        const int c1 = (p1 - c0) < kIdChunk ? p1 : c0 + kIdChunk;
-        __syncwarp();
-#pragma unroll 8
-        for (int i = lane; i < c1 - c0; i += 32) s_ids[i] = __ldg(trow + c0 + i);
-        __syncwarp();
-        for (int k0 = c0; k0 < c1; k0 += C::TK, ++it) {
-          const int ntok = (c1 - k0) < C::TK ? (c1 - k0) : C::TK;
-          const int stg = it % C::STAGES;
-          if (it >= C::STAGES) mbar_wait(&empty[stg], ((it / C::STAGES) & 1) ^ 1);
-          // Programmatic dependent launch: pages of earlier tokens were written
-          // by earlier steps, so they stream while the preceding RoPE+store
-          // kernel still runs; only a stage holding this step's fresh keys
-          // (>= the segment start) waits for that kernel to finish.
-          if (!waited && k0 + ntok > fresh) {
-            griddep_wait();
-            waited = true;
-          }
-          if (lane == 0) mbar_arrive_expect_tx(&full[stg], 2 * C::TK * C::ROW_BYTES);
-          __syncwarp();
-          const int row = lane & (C::TK - 1);
-          const int32_t page = s_ids[k0 - c0 + (row < ntok ? row : ntok - 1)];  // pad rows repeat a valid row
-          uint8_t* base = smem + stg * C::STAGE_BYTES + (lane >= C::TK ? C::TK * C::ROW_STRIDE : 0);
-          const __nv_bfloat16* src = (lane >= C::TK ? vl : kl) + (int64_t)page * (HKV * D) + hoff;
-          bulk_g2s(base + row * C::ROW_STRIDE, src, C::ROW_BYTES, &full[stg]);
+    // chunk cursor: tile r (lane-batch index i), token range [c0, c1) of its piece [.., p1)
+    int r = r0, i = 0, c0 = 0, c1 = 0, p1 = 0;
+    auto open_tile = [&](int rr) -> bool {     // position the cursor on tile rr's piece
+      if (rr >= n_dec) return false;
+      if (rr - rb >= 31) {
+        rb = rr;
+        tl.load(prefix, dec, n_dec, rb, lane);
+      }
+      const int ii = rr - rb;
+      const int lo = TIM_SHFL(tl.lo, ii), hi = TIM_SHFL(tl.hi, ii);
+      if (lo >= end) return false;
+      r = rr;
+      i = ii;
+      c0 = (start > lo ? start : lo) - lo;
+      p1 = (end < hi ? end : hi) - lo;
+      c1 = (p1 - c0) < kIdChunk ? p1 : c0 + kIdChunk;
+      return true;
+    };
+    auto fetch = [&]() {                        // ids of the cursor's chunk -> registers
+      const int32_t* trow = tables + (int64_t)TIM_SHFL(tl.slot, i) * tstride;
+#pragma unroll
+      for (int j = 0; j < IPL; ++j) {
+        const int k = c0 + lane + 32 * j;
+        idr[j] = k < c1 ? __ldg(trow + k) : 0;
+      }
+    };
+    bool more = open_tile(r0);
+    if (more) fetch();
+    while (more) {
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < IPL; ++j) s_ids[lane + 32 * j] = idr[j];
+      __syncwarp();
+      const int cur_c0 = c0, cur_c1 = c1;
+      const int fresh = TIM_SHFL(tl.fresh, i);
+      const int64_t hoff = (int64_t)TIM_SHFL(tl.hgrp, i) * HG * D;   // head-group slice
+      // advance the cursor and start the next chunk's id loads
+      if (c1 < p1) {
+        c0 = c1;
+        c1 = (p1 - c0) < kIdChunk ? p1 : c0 + kIdChunk;
+        more = true;
+      } else {
+        more = open_tile(r + 1);
+      }
+      if (more) fetch();
+      for (int k0 = cur_c0; k0 < cur_c1; k0 += C::TK, ++it) {
+        const int ntok = (cur_c1 - k0) < C::TK ? (cur_c1 - k0) : C::TK;
+        const int stg = it % C::STAGES;
+        if (it >= C::STAGES) mbar_wait(&empty[stg], ((it / C::STAGES) & 1) ^ 1);
+        // Programmatic dependent launch: pages of earlier tokens were written
+        // by earlier steps, so they stream while the preceding RoPE+store
+        // kernel still runs; only a stage holding this step's fresh keys
+        // (>= the tile's first fresh key) waits for that kernel to finish.
+        if (!waited && k0 + ntok > fresh) {
+          griddep_wait();
+          waited = true;
         }
+        if (lane == 0) mbar_arrive_expect_tx(&full[stg], 2 * C::TK * C::ROW_BYTES);
+        __syncwarp();
+        const int row = lane & (C::TK - 1);
+        const int32_t page = s_ids[k0 - cur_c0 + (row < ntok ? row : ntok - 1)];  // pad rows repeat a valid row
+        uint8_t* base = smem + stg * C::STAGE_BYTES + (lane >= C::TK ? C::TK * C::ROW_STRIDE : 0);
+        const __nv_bfloat16* src = (lane >= C::TK ? vl : kl) + (int64_t)page * (HKV * D) + hoff;
+        bulk_g2s(base + row * C::ROW_STRIDE, src, C::ROW_BYTES, &full[stg]);
       }
     }
     return;
@@ -177,22 +329,61 @@ __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
   const int64_t slot_floats = (int64_t)8 * 16 * D;     // one partial: 16 rows x <= 8 warps
   float* ws_o = ws;
   float* ws_ml = ws + (int64_t)(gridDim.x + max_dec) * slot_floats;
-  int it = 0;
+  int it = 0, rb = r0;
+  int split_first = -1, split_last = -1;   // tiles this warp left partials for
+  int old_first = 0, old_last = 0;         // their arrival counts (lane 0)
+  bool first_sent = false;
 
-  for (int r = r0; r < n_dec && prefix[r] < end; ++r) {
-    const int64_t lo = prefix[r], hi = prefix[r + 1];
-    const int p0 = (int)((start > lo ? start : lo) - lo);
-    const int p1 = (int)((end < hi ? end : hi) - lo);
-    const int32_t* rec = dec + r * TIM_DEC_FIELDS;
-    const int qrow = rec[0], kv_len = rec[2], nq = rec[3];
-    const int kvh = rec[5] * HG + hloc;      // this warp's kv head
+  // q fragments of a tile for this warp (the A operand of S = Q K^T).  The
+  // next tile's fragments are fetched into the same registers as soon as the
+  // last QK^T of the current tile has consumed them, so their latency hides
+  // behind that stage's softmax / PV and the epilogue (9 warps leave 168
+  // registers per thread: no room for a second buffer).
+  uint32_t qa[C::KC][4];
+  auto load_q = [&](uint32_t (&dst)[C::KC][4], int ii) {
+    const int qrow = TIM_SHFL(tl.qrow, ii), nq = TIM_SHFL(tl.nq, ii);
+    const int kvh = TIM_SHFL(tl.hgrp, ii) * HG + hloc;
+    int nw_q = nq - sub * qpw;
+    nw_q = nw_q < 0 ? 0 : (nw_q > qpw ? qpw : nw_q);
+    const int nrows = nw_q * grp;
+    int orow[2];
+    bool valid[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int rr = g + 8 * h;
+      valid[h] = rr < nrows;
+      orow[h] = (qrow + sub * qpw + rr / grp) * hq + kvh * grp + (rr % grp);
+    }
+#pragma unroll
+    for (int kc = 0; kc < C::KC; ++kc) {
+      const int d0 = kc * 16 + 2 * t;
+      dst[kc][0] = valid[0] ? *reinterpret_cast<const uint32_t*>(q + (int64_t)orow[0] * D + d0) : 0u;
+      dst[kc][1] = valid[1] ? *reinterpret_cast<const uint32_t*>(q + (int64_t)orow[1] * D + d0) : 0u;
+      dst[kc][2] = valid[0] ? *reinterpret_cast<const uint32_t*>(q + (int64_t)orow[0] * D + d0 + 8) : 0u;
+      dst[kc][3] = valid[1] ? *reinterpret_cast<const uint32_t*>(q + (int64_t)orow[1] * D + d0 + 8) : 0u;
+    }
+  };
+  load_q(qa, 0);
+
+  for (int r = r0; r < n_dec; ++r) {
+    if (r - rb == 31) {        // keep tiles r and r + 1 in the lane batch
+      rb = r;
+      tl.load(prefix, dec, n_dec, rb, lane);
+    }
+    const int i = r - rb;
+    const int lo = TIM_SHFL(tl.lo, i), hi = TIM_SHFL(tl.hi, i);
+    if (lo >= end) break;
+    const int p0 = (start > lo ? start : lo) - lo;
+    const int p1 = (end < hi ? end : hi) - lo;
+    const int qrow = TIM_SHFL(tl.qrow, i), kv_len = TIM_SHFL(tl.kv_len, i), nq = TIM_SHFL(tl.nq, i);
+    const int kvh = TIM_SHFL(tl.hgrp, i) * HG + hloc;      // this warp's kv head
     int nw_q = nq - sub * qpw;               // queries of this warp in the tile
     nw_q = nw_q < 0 ? 0 : (nw_q > qpw ? qpw : nw_q);
     const int nrows = nw_q * grp;
+    const bool has_next = r + 1 < n_dec && TIM_SHFL(tl.lo, i + 1) < end;
 
     int lim[2], orow[2];
     bool valid[2];
-    uint32_t qa[C::KC][4];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int rr = g + 8 * h;
@@ -201,18 +392,10 @@ __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
       lim[h] = kv_len - nq + qi;                          // last visible key (absolute)
       orow[h] = (qrow + qi) * hq + kvh * grp + (rr % grp);
     }
-#pragma unroll
-    for (int kc = 0; kc < C::KC; ++kc) {
-      const int d0 = kc * 16 + 2 * t;
-      qa[kc][0] = valid[0] ? *reinterpret_cast<const uint32_t*>(q + (int64_t)orow[0] * D + d0) : 0u;
-      qa[kc][1] = valid[1] ? *reinterpret_cast<const uint32_t*>(q + (int64_t)orow[1] * D + d0) : 0u;
-      qa[kc][2] = valid[0] ? *reinterpret_cast<const uint32_t*>(q + (int64_t)orow[0] * D + d0 + 8) : 0u;
-      qa[kc][3] = valid[1] ? *reinterpret_cast<const uint32_t*>(q + (int64_t)orow[1] * D + d0 + 8) : 0u;
-    }
 
     float o[C::NT][4];
 #pragma unroll
-    for (int i = 0; i < C::NT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    for (int j = 0; j < C::NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
     float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
 
     for (int k0 = p0; k0 < p1; k0 += C::TK, ++it) {
@@ -236,6 +419,7 @@ __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
           mma_bf16(s1, qa[kc][0], qa[kc][1], qa[kc][2], qa[kc][3], b2, b3);
         }
       }
+      if (has_next && k0 + C::TK >= p1) load_q(qa, i + 1);
       // online softmax (log2 domain); row g -> v[0], row g+8 -> v[1]
       float v[2][4] = {{s0[0], s0[1], s1[0], s1[1]}, {s0[2], s0[3], s1[2], s1[3]}};
       const int tk[4] = {2 * t, 2 * t + 1, 8 + 2 * t, 9 + 2 * t};
@@ -266,11 +450,11 @@ __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
       // after the first tiles of a query this is rare, and it is 64 FMULs.
       if (__any_sync(0xffffffffu, corr[0] != 1.f || corr[1] != 1.f)) {
 #pragma unroll
-        for (int i = 0; i < C::NT; ++i) {
-          o[i][0] *= corr[0];
-          o[i][1] *= corr[0];
-          o[i][2] *= corr[1];
-          o[i][3] *= corr[1];
+        for (int j = 0; j < C::NT; ++j) {
+          o[j][0] *= corr[0];
+          o[j][1] *= corr[0];
+          o[j][2] *= corr[1];
+          o[j][3] *= corr[1];
         }
       }
       const uint32_t pa0 = pack_bf16(v[0][0], v[0][1]);
@@ -295,116 +479,76 @@ __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
 
     if (trace && threadIdx.x == 0) trace[4 * blockIdx.x + 2] = gtimer();
     // ------------------------------------------------------------ epilogue
-    // Per warp (= per kv-head group), no CTA barrier: a tile covered by one
-    // CTA is written directly; otherwise the warp stores its unnormalised
-    // partial (O, m, l per row) and bumps the (tile, kv head) counter with an
-    // acq_rel atomic; the warp that arrives last merges the partials (K6).
+    // Per warp, no barrier and no wait: a tile covered by one CTA is written
+    // directly; otherwise the warp stores its unnormalised partial (O, m, l
+    // per row) with fire-and-forget stores and moves on.  Only a CTA's first
+    // and last tiles can be split; their arrival counters are bumped after
+    // the stream (below), when the stores have long drained, so the ring never
+    // waits on an atomic round trip.
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 1);
       l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 2);
     }
-    const int64_t c_first = cta_of(lo, G, N), c_last = cta_of(hi - 1, G, N);
-    const int npieces = (int)(c_last - c_first + 1);
-    if (npieces == 1) {
+    if (cta_of(lo, G, N) == cta_of(hi - 1, G, N)) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (valid[h]) {
           const float inv = 1.f / l_r[h];
           __nv_bfloat16* ob = out + (int64_t)orow[h] * D;
 #pragma unroll
-          for (int i = 0; i < C::NT; ++i)
-            *reinterpret_cast<uint32_t*>(ob + i * 8 + 2 * t) =
-                pack_bf16(o[i][2 * h] * inv, o[i][2 * h + 1] * inv);
+          for (int j = 0; j < C::NT; ++j)
+            *reinterpret_cast<uint32_t*>(ob + j * 8 + 2 * t) =
+                pack_bf16(o[j][2 * h] * inv, o[j][2 * h + 1] * inv);
         }
       }
       continue;
     }
     if (nrows == 0) continue;
-    const int64_t wslot = ((c + r) * 8 + warp) * 16;     // first of this warp's 16 partial rows
+    // The arrival for the CTA's first split tile goes out before the last
+    // tile's partial stores, so its release fence has nothing left to drain.
+    if (!has_next && split_first >= 0 && lane == 0) {
+      old_first = atom_add_acq_rel(counters + (int64_t)split_first * 8 + warp);
+      first_sent = true;
+    }
+    if (r == r0) split_first = r; else split_last = r;
+    const int64_t wslot = ((int64_t)(c + r) * 8 + warp) * 16;   // first of this warp's 16 partial rows
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int rr = g + 8 * h;
       if (valid[h]) {
         float* ob = ws_o + (wslot + rr) * D;
 #pragma unroll
-        for (int i = 0; i < C::NT; ++i)
-          __stcg(reinterpret_cast<float2*>(ob + i * 8 + 2 * t), make_float2(o[i][2 * h], o[i][2 * h + 1]));
+        for (int j = 0; j < C::NT; ++j)
+          __stcg(reinterpret_cast<float2*>(ob + j * 8 + 2 * t), make_float2(o[j][2 * h], o[j][2 * h + 1]));
         if (t == 0) __stcg(reinterpret_cast<float2*>(ws_ml + (wslot + rr) * 2), make_float2(m_r[h], l_r[h]));
       }
     }
-    __syncwarp();
+  }
+  // Arrivals for the split tiles (acq_rel: publishes this warp's partials and,
+  // for the last piece to arrive, acquires everyone else's); the warp that
+  // completes a (tile, warp) pair merges it (K6) and re-arms its counter.
+  // Both atomics are in flight together.
+  if (lane == 0) {
+    if (split_first >= 0 && !first_sent) old_first = atom_add_acq_rel(counters + (int64_t)split_first * 8 + warp);
+    if (split_last >= 0) old_last = atom_add_acq_rel(counters + (int64_t)split_last * 8 + warp);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int r = k == 0 ? split_first : split_last;
+    if (r < 0) continue;
+    const int lo = __ldg(prefix + r), hi = __ldg(prefix + r + 1);
+    const int c_first = (int)cta_of(lo, G, N), c_last = (int)cta_of(hi - 1, G, N);
     int last = 0;
     if (lane == 0) {
-      int old;
-      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
-                   : "=r"(old) : "l"(counters + (int64_t)r * 8 + warp) : "memory");
-      last = old == npieces - 1;
+      last = (k == 0 ? old_first : old_last) == c_last - c_first;
       if (last) counters[(int64_t)r * 8 + warp] = 0;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (!last) continue;
-    // K6 for this warp's rows: out = sum_p exp2(m_p - M) O_p / sum_p exp2(m_p - M) l_p.
-    // Rows are merged 4 at a time and partials kFastPieces at a time with an
-    // online (running-max) merge; every load of a chunk is issued before any
-    // use, so a decode tile over <= kFastPieces partials costs one round trip.
-    for (int r0w = 0; r0w < nrows; r0w += 4) {
-      float M[4], den[4];
-      float4 acc[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        M[k] = -INFINITY;
-        den[k] = 0.f;
-        acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      for (int64_t cb = c_first; cb <= c_last; cb += kFastPieces) {
-        float2 ml[4][kFastPieces];
-        float4 ov[4][kFastPieces];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-#pragma unroll
-          for (int p = 0; p < kFastPieces; ++p) {
-            ml[k][p] = make_float2(-INFINITY, 0.f);
-            ov[k][p] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (r0w + k < nrows && cb + p <= c_last) {
-              const int64_t pr = ((cb + p + r) * 8 + warp) * 16 + r0w + k;
-              ml[k][p] = __ldcg(reinterpret_cast<const float2*>(ws_ml + pr * 2));
-              if (lane * 4 < D) ov[k][p] = __ldcg(reinterpret_cast<const float4*>(ws_o + pr * D) + lane);
-            }
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          float mc = M[k];
-#pragma unroll
-          for (int p = 0; p < kFastPieces; ++p) mc = fmaxf(mc, ml[k][p].x);
-          const float sc = M[k] == -INFINITY ? 0.f : fast_exp2(M[k] - mc);
-          den[k] *= sc;
-          acc[k].x *= sc; acc[k].y *= sc; acc[k].z *= sc; acc[k].w *= sc;
-#pragma unroll
-          for (int p = 0; p < kFastPieces; ++p) {
-            const float w = ml[k][p].x == -INFINITY ? 0.f : fast_exp2(ml[k][p].x - mc);
-            den[k] += w * ml[k][p].y;
-            acc[k].x += w * ov[k][p].x; acc[k].y += w * ov[k][p].y;
-            acc[k].z += w * ov[k][p].z; acc[k].w += w * ov[k][p].w;
-          }
-          M[k] = mc;
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int rr = r0w + k;
-        if (rr < nrows && lane * 4 < D) {
-          const int qi = sub * qpw + rr / grp;
-          const int64_t oidx = (int64_t)(qrow + qi) * hq + kvh * grp + (rr % grp);
-          const float inv = 1.f / den[k];
-          uint2 pk;
-          pk.x = pack_bf16(acc[k].x * inv, acc[k].y * inv);
-          pk.y = pack_bf16(acc[k].z * inv, acc[k].w * inv);
-          *reinterpret_cast<uint2*>(out + oidx * D + lane * 4) = pk;
-        }
-      }
-    }
+    const int32_t* rec = dec + (int64_t)r * TIM_DEC_FIELDS;
+    merge_pieces<D, HKV, HG, WPH>(ws_o, ws_ml, out, r, warp, c_first, c_last, __ldg(rec + 0),
+                                  __ldg(rec + 3), __ldg(rec + 5), hq, lane);
   }
   if (trace && threadIdx.x == 0) trace[4 * blockIdx.x + 3] = gtimer();
 }
@@ -489,20 +633,20 @@ int32_t launch_tiles(const int32_t* step, int list, const void* q, void* out, co
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_ctas);
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attrs[1];
-  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attrs[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(
-      &cfg, kern, step, list, (const __nv_bfloat16*)q, (__nv_bfloat16*)out,
-      (const __nv_bfloat16*)kl, (const __nv_bfloat16*)vl, tables, tstride, hq, scale, ws, counters,
-      max_dec);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, step, list, (const __nv_bfloat16*)q,
+                                           (__nv_bfloat16*)out, (const __nv_bfloat16*)kl,
+                                           (const __nv_bfloat16*)vl, tables, tstride, hq, scale,
+                                           ws, counters, max_dec);
   if (e != cudaSuccess) {
     set_last_error("attn_tiles launch: %s", cudaGetErrorString(e));
     return TIM_CUDA_ERROR;
@@ -578,12 +722,10 @@ extern "C" int32_t tim_attn_decode(const int32_t* step, int32_t mode, const void
   if (head_dim == DD && hkv == HH) {                                                           \
     if (mode == 0)                                                                             \
       return launch_tiles<DD, HH, HH, 1>(step, 0, q, out, k_layer, v_layer, block_tables,      \
-                                         table_stride, hq, scale, ws, counters, n_ctas,        \
-                                         max_dec, st);                                         \
+                                         table_stride, hq, scale, ws, counters, n_ctas, max_dec, st); \
     return launch_tiles<DD, HH, ext_hg(HH), 8 / ext_hg(HH)>(step, 1, q, out, k_layer, v_layer, \
                                                             block_tables, table_stride, hq,    \
-                                                            scale, ws, counters, n_ctas,       \
-                                                            max_dec, st);                      \
+                                                            scale, ws, counters, n_ctas, max_dec, st); \
   }
   TIM_TILES(128, 8) TIM_TILES(128, 4) TIM_TILES(128, 2) TIM_TILES(128, 1)
   TIM_TILES(64, 8) TIM_TILES(64, 4) TIM_TILES(64, 2) TIM_TILES(64, 1)

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--dump", action="store_true")
     a = ap.parse_args()
     hq, hkv, d = 32, 8, 128
     rng = np.random.default_rng(0)
@@ -83,6 +84,13 @@ def main():
         t = (t - t0) / 1000.0
         print(json.dumps({k: [round(float(np.percentile(t[:, i], p)), 2) for p in (0, 50, 100)]
                           for i, k in enumerate(["start", "first", "loop_end", "end"])}))
+        if a.dump:
+            pre = np.concatenate([[0], np.cumsum(lens)])
+            N = int(pre[-1])
+            for c in range(ctas):
+                s0, s1 = c * N // ctas, (c + 1) * N // ctas
+                nseg = int(np.searchsorted(pre, s1, side="left") - np.searchsorted(pre, s0, side="right") + 1)
+                print(c, nseg, " ".join(f"{x:7.2f}" for x in t[c]))
     byts = int(lens.sum()) * hkv * d * 2 * 2 + a.batch * hq * d * 2 * 2
     ms = float(np.median(times))
     print(json.dumps({"tokens": int(lens.sum()), "bytes": byts, "ms": ms,

@@ -170,12 +170,15 @@ int32_t tim_attn_decode(const int32_t* step, int32_t mode, const void* q, void* 
                         int32_t dtype, void* stream);
 /* Queries per multi-token tile and kv-head groups per query for a config. */
 int32_t tim_extend_queries_per_item(int32_t hq, int32_t hkv, int32_t head_dim, int32_t dtype);
-int32_t tim_extend_head_groups(int32_t hkv);
+int32_t tim_extend_head_groups(int32_t hq, int32_t hkv, int32_t head_dim);
 
 /* Diagnostics: per-CTA %globaltimer timeline of tim_attn_decode written to
  * buf[4*cta .. 4*cta+3] = {start, first stage landed, main loop end, end};
  * pass NULL to disable. */
 int32_t tim_set_trace(void* buf);
+/* Diagnostics: per-64-key-block %globaltimer stamps of CTA 0 of the tcgen05
+ * multi-token kernel, buf[8*block + {0..5}]; NULL disables. */
+int32_t tim_tc_trace(void* buf);
 
 /* Reference-precision attention (fp32, or shapes outside the tensor-core
  * kernel): every row of the step's segments attends its paged prefix plus the

@@ -52,9 +52,10 @@ SIGNATURES = {
                                _i32, _i32, _i32, _p]),
     "tim_attn_extend": (_i32, [_p, _i32, _p, _p, _p, _p, _p, _i64, _i32, _i32, _i32, _f32, _i32, _p]),
     "tim_extend_queries_per_item": (_i32, [_i32, _i32, _i32, _i32]),
-    "tim_extend_head_groups": (_i32, [_i32]),
+    "tim_extend_head_groups": (_i32, [_i32, _i32, _i32]),
     "tim_argmax": (_i32, [_p, _i32, _i32, _p, _i32, _p]),
     "tim_set_trace": (_i32, [_p]),
+    "tim_tc_trace": (_i32, [_p]),
     "tim_tmap_2d_bf16": (_i32, [_p, _p, _i64, _i64, _i32, _i32]),
     "tim_gemm_ws_floats": (_i64, [_i32, _i32]),
     "tim_gemm_skinny": (_i32, [_p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _i32, _p]),

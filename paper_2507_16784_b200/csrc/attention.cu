@@ -27,6 +27,11 @@
 
 namespace tim {
 
+bool ext_tc_shape(int hq, int hkv, int head_dim);
+int32_t launch_ext_tc(const int32_t* step, const void* q, void* out, const void* kl, const void* vl,
+                      const int32_t* tables, int64_t tstride, int hq, int hkv, float scale,
+                      int n_ctas, cudaStream_t st);
+
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kIdChunk = 512;       // page ids staged per producer refill (multiple of TK)
 constexpr int kFastPieces = 4;      // partials merged per round trip by K6
@@ -212,11 +217,15 @@ __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
   const int n_dec = list ? hd.n_ext : hd.n_dec;
   const int N = list ? hd.ext_total : hd.dec_total;
-  if (n_dec == 0 || N == 0) return;
   const int want = (N + kMinTokensPerCta - 1) / kMinTokensPerCta;
   const int G = (int)gridDim.x < want ? (int)gridDim.x : want;
   const int c = blockIdx.x;
-  if (c >= G) return;
+  if (n_dec == 0 || N == 0 || c >= G) {
+    // An idle CTA still waits for the preceding grid, so that this grid's
+    // completion implies it (the next PDL launch relies on the chain).
+    griddep_wait();
+    return;
+  }
   const int32_t* dec = step + (list ? hd.off_ext : hd.off_dec);
   const int32_t* prefix = step + (list ? hd.off_ext_prefix : hd.off_dec_prefix);
   const int start = (int)((int64_t)c * N / G), end = (int)((int64_t)(c + 1) * N / G);
@@ -676,12 +685,16 @@ extern "C" int64_t tim_decode_ws_floats(int32_t n_ctas, int32_t max_dec, int32_t
 
 extern "C" int32_t tim_extend_queries_per_item(int32_t hq, int32_t hkv, int32_t head_dim, int32_t dtype) {
   // queries per multi-token attention tile (mode 1 of tim_attn_decode)
+  if (dtype == TIM_DTYPE_BF16 && ext_tc_shape(hq, hkv, head_dim)) return 128 / (hq / hkv);
   if (dtype == TIM_DTYPE_BF16 && tensor_core_shape(hq, hkv, head_dim))
     return (8 / ext_hg(hkv)) * (16 / (hq / hkv));
   return 1 << 30;  // generic path: whole segments
 }
 
-extern "C" int32_t tim_extend_head_groups(int32_t hkv) { return hkv / ext_hg(hkv); }
+extern "C" int32_t tim_extend_head_groups(int32_t hq, int32_t hkv, int32_t head_dim) {
+  if (ext_tc_shape(hq, hkv, head_dim)) return hkv;   // one tcgen05 item per kv head
+  return hkv / ext_hg(hkv);
+}
 
 static int32_t launch_generic(const int32_t* step, int32_t n_rows, const void* q, void* out,
                               const void* kl, const void* vl, const int32_t* tables,
@@ -727,6 +740,9 @@ extern "C" int32_t tim_attn_decode(const int32_t* step, int32_t mode, const void
                                                             block_tables, table_stride, hq,    \
                                                             scale, ws, counters, n_ctas, max_dec, st); \
   }
+  if (mode == 1 && ext_tc_shape(hq, hkv, head_dim))   // multi-token tiles on tcgen05 (attention_tc.cu)
+    return launch_ext_tc(step, q, out, k_layer, v_layer, block_tables, table_stride, hq, hkv, scale,
+                         n_ctas, st);
   TIM_TILES(128, 8) TIM_TILES(128, 4) TIM_TILES(128, 2) TIM_TILES(128, 1)
   TIM_TILES(64, 8) TIM_TILES(64, 4) TIM_TILES(64, 2) TIM_TILES(64, 1)
 #undef TIM_TILES

@@ -16,114 +16,211 @@ TIM_DEV Vec<T> ldv(const T* p) { return *reinterpret_cast<const Vec<T>*>(p); }
 template <typename T>
 TIM_DEV void stv(T* p, const Vec<T>& x) { *reinterpret_cast<Vec<T>*>(p) = x; }
 
-// 1 / sqrt(mean(h_row^2) + eps) of one row, all threads of the CTA get it.
 // Weightless RMSNorm commutes with the following GEMM (rms(h) @ W ==
 // (h @ W) / rms_scale), so the forward runs its GEMMs on the raw residual
-// stream and applies this per-row scale in the consumer kernel (model.py:69-70).
-template <typename T>
-TIM_DEV float row_inv_rms(const T* __restrict__ h, int dm, float eps) {
-  constexpr int V = Vec<T>::V;
-  __shared__ float red[32];
-  float acc = 0.f;
-  for (int e = threadIdx.x * V; e < dm; e += blockDim.x * V) {
-    const Vec<T> x = ldv(h + e);
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      const float f = to_f32(x.v[k]);
-      acc += f * f;
-    }
-  }
-  acc = warp_sum(acc);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+// stream and applies the per-row scale in the consumer kernel (model.py:69-70).
+
+// Block-wide sum of one float per thread (every thread gets the total).
+template <int NT>
+TIM_DEV float block_sum(float v) {
+  __shared__ float red[NT / 32];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
   float tot = 0.f;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
-  __syncthreads();
-  return 1.f / sqrtf(tot / (float)dm + eps);
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) tot += red[w];
+  return tot;
 }
 
-// K3: RoPE + page store, fused with the preceding RMSNorm scale.  Grid
-// (rows, splits); the row's work items (rotated q/k vectors, v vectors) are
-// divided over the splits.  qkv row layout: [q heads | k heads | v heads] x D,
-// the column order of the fused [wq | wk | wv] GEMM.  Rotate-half convention
-// (model.py:118-125): out[i] = x1*cos - x2*sin, out[i+half] = x1*sin + x2*cos.
-template <typename T>
-__global__ void __launch_bounds__(128)
+// K3: RoPE + page store, fused with the preceding RMSNorm scale.  One CTA per
+// row; every global load of the row (the residual h for the RMS scale, the
+// q/k halves and v vectors, cos/sin) is issued before the block reduction, so
+// the kernel costs one memory round trip.  qkv row layout: [q heads | k heads
+// | v heads] x D, the column order of the fused [wq | wk | wv] GEMM.
+// Rotate-half convention (model.py:118-125): out[i] = x1*cos - x2*sin,
+// out[i+half] = x1*sin + x2*cos.  Items beyond NT*MAXI per row (larger
+// models) take a second, unbuffered pass.
+template <typename T, int NT, int MAXI>
+__global__ void __launch_bounds__(NT)
     rope_kv_kernel(const T* __restrict__ qkv, const T* __restrict__ h, int dm, float eps,
                    const int32_t* __restrict__ row_pos, const int32_t* __restrict__ row_pages,
                    const float* __restrict__ cos_tab, const float* __restrict__ sin_tab, int hq,
                    int hkv, int D, T* __restrict__ q_out, T* __restrict__ k_layer,
                    T* __restrict__ v_layer) {
   constexpr int V = Vec<T>::V;
-  griddep_launch();   // the attention kernel may start staging its page ids now
+  constexpr int MAXH = 4;
+  griddep_launch();   // the attention kernel may start streaming old pages now
   const int r = blockIdx.x;
-  const float inv = h ? row_inv_rms(h + (int64_t)r * dm, dm, eps) : 1.f;
   const int half = D >> 1;
   const int gph = half / V;                       // rope vector groups per head
   const int n_rope = (hq + hkv) * gph;
-  const int n_v = hkv * D / V;
-  const int total = n_rope + n_v;
-  const int per = (total + gridDim.y - 1) / gridDim.y;
-  const int i0 = blockIdx.y * per, i1 = min(total, i0 + per);
+  const int total = n_rope + hkv * D / V;
   const int pos = row_pos[r];
   const int page = row_pages[r];
   const T* x = qkv + (int64_t)r * (hq + 2 * hkv) * D;
   const float* ct = cos_tab + (int64_t)pos * half;
   const float* st = sin_tab + (int64_t)pos * half;
-  for (int it = i0 + threadIdx.x; it < i1; it += blockDim.x) {
+  const T* hr = h ? h + (int64_t)r * dm : nullptr;
+
+  Vec<T> hv[MAXH], av[MAXI], bv[MAXI];
+  float cs[MAXI][V], sn[MAXI][V];
+#pragma unroll
+  for (int k = 0; k < MAXH; ++k) {
+    const int e = (threadIdx.x + k * NT) * V;
+    if (hr && e < dm) hv[k] = ldv(hr + e);
+  }
+#pragma unroll
+  for (int k = 0; k < MAXI; ++k) {
+    const int it = threadIdx.x + k * NT;
     if (it < n_rope) {
       const int head = it / gph, c = (it - head * gph) * V;
-      const T* src = x + head * D;
-      const Vec<T> a = ldv(src + c), b = ldv(src + half + c);
+      av[k] = ldv(x + head * D + c);
+      bv[k] = ldv(x + head * D + half + c);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        cs[k][j] = ct[c + j];
+        sn[k][j] = st[c + j];
+      }
+    } else if (it < total) {
+      av[k] = ldv(x + (hq + hkv) * D + (it - n_rope) * V);
+    }
+  }
+  float inv = 1.f;
+  if (hr) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < MAXH; ++k) {
+      const int e = (threadIdx.x + k * NT) * V;
+      if (e < dm) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const float f = to_f32(hv[k].v[j]);
+          acc += f * f;
+        }
+      }
+    }
+    for (int e = (threadIdx.x + MAXH * NT) * V; e < dm; e += NT * V) {   // dm > NT*V*MAXH
+      const Vec<T> y = ldv(hr + e);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc += to_f32(y.v[j]) * to_f32(y.v[j]);
+    }
+    inv = 1.f / sqrtf(block_sum<NT>(acc) / (float)dm + eps);
+  }
+  auto emit = [&](int it, const Vec<T>& a, const Vec<T>& b, const float* c_, const float* s_) {
+    if (it < n_rope) {
+      const int head = it / gph, c = (it - head * gph) * V;
       Vec<T> o1, o2;
 #pragma unroll
-      for (int k = 0; k < V; ++k) {
-        const float x1 = to_f32(a.v[k]) * inv, x2 = to_f32(b.v[k]) * inv;
-        const float cs = ct[c + k], sn = st[c + k];
-        o1.v[k] = from_f32<T>(x1 * cs - x2 * sn);
-        o2.v[k] = from_f32<T>(x1 * sn + x2 * cs);
+      for (int j = 0; j < V; ++j) {
+        const float x1 = to_f32(a.v[j]) * inv, x2 = to_f32(b.v[j]) * inv;
+        o1.v[j] = from_f32<T>(x1 * c_[j] - x2 * s_[j]);
+        o2.v[j] = from_f32<T>(x1 * s_[j] + x2 * c_[j]);
       }
       T* dst;
       if (head < hq) {
         dst = q_out + ((int64_t)r * hq + head) * D;
       } else {
-        if (page < 0) continue;
+        if (page < 0) return;
         dst = k_layer + ((int64_t)page * hkv + (head - hq)) * D;
       }
       stv(dst + c, o1);
       stv(dst + half + c, o2);
     } else if (page >= 0) {
-      const int e = (it - n_rope) * V;
-      const Vec<T> a = ldv(x + (hq + hkv) * D + e);
       Vec<T> o;
 #pragma unroll
-      for (int k = 0; k < V; ++k) o.v[k] = from_f32<T>(to_f32(a.v[k]) * inv);
-      stv(v_layer + (int64_t)page * hkv * D + e, o);
+      for (int j = 0; j < V; ++j) o.v[j] = from_f32<T>(to_f32(a.v[j]) * inv);
+      stv(v_layer + (int64_t)page * hkv * D + (it - n_rope) * V, o);
     }
+  };
+#pragma unroll
+  for (int k = 0; k < MAXI; ++k) {
+    const int it = threadIdx.x + k * NT;
+    if (it < total) emit(it, av[k], bv[k], cs[k], sn[k]);
+  }
+  for (int it = threadIdx.x + MAXI * NT; it < total; it += NT) {   // rows wider than NT*MAXI items
+    Vec<T> a, b;
+    float c_[V], s_[V];
+    if (it < n_rope) {
+      const int head = it / gph, c = (it - head * gph) * V;
+      a = ldv(x + head * D + c);
+      b = ldv(x + head * D + half + c);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        c_[j] = ct[c + j];
+        s_[j] = st[c + j];
+      }
+    } else {
+      a = ldv(x + (hq + hkv) * D + (it - n_rope) * V);
+    }
+    emit(it, a, b, c_, s_);
   }
 }
 
 // u = silu(u * inv_rms(h_row)) in place: the MLP input RMSNorm folded behind
-// the W1 GEMM (model.py:161), grid (rows, splits).
-template <typename T>
-__global__ void __launch_bounds__(128)
+// the W1 GEMM (model.py:161).  One CTA per row, all loads issued before the
+// reduction (one round trip); widths beyond NT*V*MAXU take a second pass.
+template <typename T, int NT, int MAXU>
+__global__ void __launch_bounds__(NT)
     silu_rms_kernel(T* __restrict__ u, int width, const T* __restrict__ h, int dm, float eps) {
   constexpr int V = Vec<T>::V;
+  constexpr int MAXH = 4;
   griddep_launch();   // the down-projection GEMM may start streaming its weights
   const int r = blockIdx.x;
-  const float inv = h ? row_inv_rms(h + (int64_t)r * dm, dm, eps) : 1.f;
-  const int nv = width / V;
-  const int per = (nv + gridDim.y - 1) / gridDim.y;
-  const int i0 = blockIdx.y * per, i1 = min(nv, i0 + per);
   T* row = u + (int64_t)r * width;
-  for (int it = i0 + threadIdx.x; it < i1; it += blockDim.x) {
-    Vec<T> a = ldv(row + it * V);
+  const T* hr = h ? h + (int64_t)r * dm : nullptr;
+  Vec<T> hv[MAXH], uv[MAXU];
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      const float f = to_f32(a.v[k]) * inv;
-      a.v[k] = from_f32<T>(f / (1.0f + expf(-f)));
+  for (int k = 0; k < MAXH; ++k) {
+    const int e = (threadIdx.x + k * NT) * V;
+    if (hr && e < dm) hv[k] = ldv(hr + e);
+  }
+#pragma unroll
+  for (int k = 0; k < MAXU; ++k) {
+    const int e = (threadIdx.x + k * NT) * V;
+    if (e < width) uv[k] = ldv(row + e);
+  }
+  float inv = 1.f;
+  if (hr) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < MAXH; ++k) {
+      const int e = (threadIdx.x + k * NT) * V;
+      if (e < dm) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const float f = to_f32(hv[k].v[j]);
+          acc += f * f;
+        }
+      }
     }
-    stv(row + it * V, a);
+    for (int e = (threadIdx.x + MAXH * NT) * V; e < dm; e += NT * V) {
+      const Vec<T> y = ldv(hr + e);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc += to_f32(y.v[j]) * to_f32(y.v[j]);
+    }
+    inv = 1.f / sqrtf(block_sum<NT>(acc) / (float)dm + eps);
+  }
+#pragma unroll
+  for (int k = 0; k < MAXU; ++k) {
+    const int e = (threadIdx.x + k * NT) * V;
+    if (e < width) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const float f = to_f32(uv[k].v[j]) * inv;
+        uv[k].v[j] = from_f32<T>(f / (1.0f + expf(-f)));
+      }
+      stv(row + e, uv[k]);
+    }
+  }
+  for (int e = (threadIdx.x + MAXU * NT) * V; e < width; e += NT * V) {
+    Vec<T> a = ldv(row + e);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const float f = to_f32(a.v[j]) * inv;
+      a.v[j] = from_f32<T>(f / (1.0f + expf(-f)));
+    }
+    stv(row + e, a);
   }
 }
 
@@ -222,10 +319,7 @@ extern "C" int32_t tim_rope_kv_store(const void* qkv, const void* h, int32_t dm,
     set_last_error("rope_kv_store: head_dim must be a multiple of %d and dm of %d", 2 * V, V);
     return TIM_BAD_ARGUMENT;
   }
-  const int items = (hq + hkv) * (head_dim / 2 / V) + hkv * head_dim / V;
-  const int splits = items > 512 ? 4 : (items > 256 ? 2 : 1);
-  dim3 grid(n_rows, splits);
-  TIM_DISPATCH(dtype, rope_kv_kernel<T><<<grid, 128, 0, (cudaStream_t)stream>>>(
+  TIM_DISPATCH(dtype, rope_kv_kernel<T, 256, 2><<<n_rows, 256, 0, (cudaStream_t)stream>>>(
                           (const T*)qkv, (const T*)h, dm, eps, row_pos, row_pages, cos_tab, sin_tab,
                           hq, hkv, head_dim, (T*)q_out, (T*)k_layer, (T*)v_layer));
   return check_launch("rope_kv_store");
@@ -239,9 +333,7 @@ extern "C" int32_t tim_silu_rms(void* u, int32_t n_rows, int32_t width, const vo
     set_last_error("silu_rms: width and dm must be multiples of %d", V);
     return TIM_BAD_ARGUMENT;
   }
-  const int splits = width / V >= 1024 ? 8 : (width / V >= 256 ? 2 : 1);
-  dim3 grid(n_rows, splits);
-  TIM_DISPATCH(dtype, silu_rms_kernel<T><<<grid, 128, 0, (cudaStream_t)stream>>>(
+  TIM_DISPATCH(dtype, silu_rms_kernel<T, 256, 6><<<n_rows, 256, 0, (cudaStream_t)stream>>>(
                           (T*)u, width, (const T*)h, dm, eps));
   return check_launch("silu_rms");
 }

@@ -385,6 +385,11 @@ class B200Transformer:
         self.tensor_cores = (cfg.precision == "bfloat16" and L.load().tim_extend_queries_per_item(
             hq, hkv, D, L.DTYPE_BF16) < (1 << 30))
         self.tile_q = 16 // (hq // hkv) if self.tensor_cores else 0   # queries per mode-0 tile
+        # multi-token rows go to the tcgen05 kernel (mode 1) when the shape has
+        # one: 128 MMA rows = ext_q queries x the q heads of one kv head
+        qpi = L.load().tim_extend_queries_per_item(hq, hkv, D, L.DTYPE_BF16) if self.tensor_cores else 0
+        self.ext_q = qpi if self.tensor_cores and qpi * (hq // hkv) == 128 else 0
+        self.ext_groups = L.load().tim_extend_head_groups(hq, hkv, D) if self.ext_q else 0
         self._runtimes: dict[int, StepRuntime] = {}
 
     @staticmethod
@@ -480,16 +485,24 @@ class B200Transformer:
         return self._forward([last_token], [position], table, pool)
 
     # ------------------------------------------------------ batched path
+    EXT_MIN_ROWS = 8
+
     def plan_attention(self, sd: StepDesc, slot: int, m: int, n: int, row_off: int) -> None:
-        """Attention work records for one segment: split-K decode for single-row
-        tensor-core segments, q-tiles for the rest."""
+        """Attention work records for one segment: decode tiles (mode 0) for
+        single rows and short segments, tcgen05 items (mode 1) for longer ones."""
         sd.segs.append((slot, m, n, row_off))
         if not self.tensor_cores:
             return
-        # Every row goes through the decode-tile kernel (mode 0): tiles of
-        # tile_q consecutive queries x all kv heads.  Measured on B200, this
-        # beats the head-grouped multi-token mode (mode 1: fewer K/V bytes per
-        # query but the same MMA-instruction count, which bounds these tiles).
+        if self.ext_q and n >= self.EXT_MIN_ROWS:
+            # re-encode / tool / prefill segment: tcgen05 items of ext_q queries
+            # x one kv head (K/V slice streamed once per ext_q queries)
+            for q0 in range(0, n, self.ext_q):
+                nq = min(self.ext_q, n - q0)
+                for g in range(self.ext_groups):
+                    sd.ext.append((row_off + q0, slot, m + q0 + nq, nq, m, g))
+            return
+        # Decode rows and short segments: the split-K decode-tile kernel (mode 0),
+        # tiles of tile_q consecutive queries x all kv heads.
         tq = self.tile_q
         for q0 in range(0, n, tq):
             nq = min(tq, n - q0)

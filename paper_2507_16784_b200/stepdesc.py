@@ -84,6 +84,8 @@ class StepDesc:
         hdr["off_dec_prefix"] = off
         parts.append(prefix.astype(np.int32))
         off += prefix.size
+        # longest items first: the kernel deals them round-robin to its CTAs
+        self.ext.sort(key=lambda e: -e[2])
         add("ext", self.ext, L.EXT_FIELDS)
         eprefix = np.zeros(len(self.ext) + 1, dtype=np.int64)
         if self.ext:

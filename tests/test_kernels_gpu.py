@@ -116,7 +116,7 @@ def test_extend_tiles_bf16_matches_oracle(hq, hkv, n_ctas):
     segs = [(0, 1), (0, 7), (5, 33), (100, 64), (700, 150), (0, 200), (1200, 3), (40, 1)]
     kp, vp, tab, stride, q, sd, rows = _extend_case(hq, hkv, d, torch.bfloat16, segs, 11)
     qpi = L.load().tim_extend_queries_per_item(hq, hkv, d, L.DTYPE_BF16)
-    ngr = L.load().tim_extend_head_groups(hkv)
+    ngr = L.load().tim_extend_head_groups(hq, hkv, d)
     assert qpi * (hq // hkv) == 16 * (8 * ngr // hkv)
     row = 0
     for i, (m, n) in enumerate(segs):

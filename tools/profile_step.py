@@ -1,5 +1,7 @@
-"""Profile one steady-state C2 engine step under ncu (profiling window only
-around the chosen step; run with `ncu --profile-from-start off ...`)."""
+"""Profile steady-state C2 engine steps under ncu (run with
+`ncu --profile-from-start off ...`): after --skip steps (same default as
+bench.py), the profiler window opens around the next step whose batched
+forward has exactly --rows rows (64 = a decode-only step; 0 = any step)."""
 import argparse
 import sys
 from pathlib import Path
@@ -12,21 +14,35 @@ import bench  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--skip", type=int, default=600)
-    ap.add_argument("--decode-only", action="store_true", help="profile the next step with 64 rows")
+    ap.add_argument("--skip", type=int, default=1500)
+    ap.add_argument("--rows", type=int, default=64)
+    ap.add_argument("--min-rows", type=int, default=0, help="profile the next step with >= this many rows")
     a = ap.parse_args()
     eng, cfg, model = bench.build_engine(0, 64, 2)
-    eng.runtime.precapture()
+    rt = eng.runtime
+    rt.precapture()
     for _ in range(a.skip):
         eng.step()
-    # find a decode-only step: plan ahead without executing would change state; instead
-    # step until the *planned* row count is 64 by peeking at the last step's rows
     torch.cuda.synchronize()
-    torch.cuda.profiler.start()
-    eng.step()
-    torch.cuda.synchronize()
-    torch.cuda.profiler.stop()
-    print("profiled one step", file=sys.stderr)
+    orig = rt.run_step
+    state = {"done": False, "rows": None}
+
+    def run_step(sd, forward=True):
+        want = (a.min_rows and sd.n_rows >= a.min_rows) or (not a.min_rows and (a.rows == 0 or sd.n_rows == a.rows))
+        if state["done"] or not forward or not want:
+            return orig(sd, forward)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        out = orig(sd, forward)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        state["done"], state["rows"] = True, sd.n_rows
+        return out
+
+    rt.run_step = run_step
+    while not state["done"]:
+        eng.step()
+    print(f"profiled one step with {state['rows']} rows", file=sys.stderr)
 
 
 if __name__ == "__main__":

@@ -68,7 +68,8 @@ typedef struct {
   int32_t off_new, off_segs, off_dec, off_dec_prefix, off_ext, off_jobs, off_spans;
   int32_t off_ops, off_phases, off_last;
   int32_t ext_total, off_ext_prefix;
-  int32_t reserved[9];
+  int32_t split_dec_ctas, split_ext_ctas;  /* mode-2 attention: CTAs on dec tiles / ext items */
+  int32_t reserved[7];
 } tim_step_header;  /* 32 int32 */
 
 #define TIM_NEW_FIELDS 5

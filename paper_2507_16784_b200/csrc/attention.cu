@@ -24,13 +24,9 @@
 // Generic (fp32 / any): warp per (row, q head), exact two-pass softmax; used
 //   for the fp32 parity configuration.
 #include "common.cuh"
+#include "attention_tc.cuh"
 
 namespace tim {
-
-bool ext_tc_shape(int hq, int hkv, int head_dim);
-int32_t launch_ext_tc(const int32_t* step, const void* q, void* out, const void* kl, const void* vl,
-                      const int32_t* tables, int64_t tstride, int hq, int hkv, float scale,
-                      int n_ctas, cudaStream_t st);
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kIdChunk = 512;       // page ids staged per producer refill (multiple of TK)
@@ -197,13 +193,13 @@ TIM_DEV void merge_pieces(const float* __restrict__ ws_o, const float* __restric
   }
 }
 
+// Body of K1 for CTA `cta` of the `grid` CTAs that stream the tile list.
 template <int D, int HKV, int HG, int WPH>
-__global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
-    attn_tiles_kernel(const int32_t* __restrict__ step, int list, const __nv_bfloat16* __restrict__ q,
-                      __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kl,
-                      const __nv_bfloat16* __restrict__ vl, const int32_t* __restrict__ tables,
-                      int64_t tstride, int hq, float scale, float* __restrict__ ws,
-                      int32_t* __restrict__ counters, int max_dec) {
+TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_bfloat16* __restrict__ q,
+                        __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kl,
+                        const __nv_bfloat16* __restrict__ vl, const int32_t* __restrict__ tables,
+                        int64_t tstride, int hq, float scale, float* __restrict__ ws,
+                        int32_t* __restrict__ counters, int max_dec, int cta, int grid) {
   using C = AttnCfg<D, HG, WPH>;
   constexpr int NW = C::NW;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -211,15 +207,14 @@ __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
   uint64_t* empty = full + C::STAGES;
   int32_t* s_ids = reinterpret_cast<int32_t*>(empty + C::STAGES);
 
-  griddep_launch();   // let the next kernel (o_proj GEMM) start prefetching its weights
   unsigned long long* trace = g_trace;
   if (trace && threadIdx.x == 0) trace[4 * blockIdx.x] = gtimer();
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
   const int n_dec = list ? hd.n_ext : hd.n_dec;
   const int N = list ? hd.ext_total : hd.dec_total;
   const int want = (N + kMinTokensPerCta - 1) / kMinTokensPerCta;
-  const int G = (int)gridDim.x < want ? (int)gridDim.x : want;
-  const int c = blockIdx.x;
+  const int G = grid < want ? grid : want;
+  const int c = cta;
   if (n_dec == 0 || N == 0 || c >= G) {
     // An idle CTA still waits for the preceding grid, so that this grid's
     // completion implies it (the next PDL launch relies on the chain).
@@ -337,7 +332,7 @@ __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
   const uint32_t smem_base = smem_u32(smem);
   const int64_t slot_floats = (int64_t)8 * 16 * D;     // one partial: 16 rows x <= 8 warps
   float* ws_o = ws;
-  float* ws_ml = ws + (int64_t)(gridDim.x + max_dec) * slot_floats;
+  float* ws_ml = ws + (int64_t)(grid + max_dec) * slot_floats;
   int it = 0, rb = r0;
   int split_first = -1, split_last = -1;   // tiles this warp left partials for
   int old_first = 0, old_last = 0;         // their arrival counts (lane 0)
@@ -562,6 +557,56 @@ __global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
   if (trace && threadIdx.x == 0) trace[4 * blockIdx.x + 3] = gtimer();
 }
 
+template <int D, int HKV, int HG, int WPH>
+__global__ void __launch_bounds__(AttnCfg<D, HG, WPH>::THREADS, 1)
+    attn_tiles_kernel(const int32_t* __restrict__ step, int list, const __nv_bfloat16* __restrict__ q,
+                      __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kl,
+                      const __nv_bfloat16* __restrict__ vl, const int32_t* __restrict__ tables,
+                      int64_t tstride, int hq, float scale, float* __restrict__ ws,
+                      int32_t* __restrict__ counters, int max_dec) {
+  griddep_launch();   // let the next kernel get resident early
+  tiles_body<D, HKV, HG, WPH>(step, list, q, out, kl, vl, tables, tstride, hq, scale, ws, counters, max_dec,
+                              blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(tc::THREADS, 1)
+    attn_ext_tc_kernel(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat16* __restrict__ vl,
+                       const int32_t* __restrict__ step, const __nv_bfloat16* __restrict__ q,
+                       __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ tables,
+                       int64_t tstride, int hq, int hkv, float scale_log2) {
+  griddep_launch();
+  ext_tc_body(kl, vl, step, q, out, tables, tstride, hq, hkv, scale_log2, blockIdx.x, gridDim.x);
+}
+
+// One launch for a whole step's attention (decode tiles + multi-token items):
+// the first split_dec_ctas CTAs stream the decode tiles (K1), the others work
+// the tcgen05 items (K2), concurrently, with the split the host derived from
+// the two lists' work (tim_step_header.split_*).  Keeps programmatic
+// dependent launch after the RoPE/store kernel, which two launches on forked
+// streams would lose.
+template <int D, int HKV>
+__global__ void __launch_bounds__(AttnCfg<D, HKV, 1>::THREADS, 1)
+    attn_step_kernel(const int32_t* __restrict__ step, const __nv_bfloat16* __restrict__ q,
+                     __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kl,
+                     const __nv_bfloat16* __restrict__ vl, const int32_t* __restrict__ tables,
+                     int64_t tstride, int hq, float scale, float* __restrict__ ws,
+                     int32_t* __restrict__ counters, int max_dec) {
+  griddep_launch();
+  const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
+  int g0 = hd.split_dec_ctas, g1 = hd.split_ext_ctas;
+  if (g0 + g1 <= 0 || g0 + g1 > (int)gridDim.x) {   // no split planned by the host
+    g0 = hd.n_ext ? (hd.n_dec ? (int)gridDim.x / 2 : 0) : (int)gridDim.x;
+    g1 = gridDim.x - g0;
+  }
+  const int c = blockIdx.x;
+  if (c < g0)
+    tiles_body<D, HKV, HKV, 1>(step, 0, q, out, kl, vl, tables, tstride, hq, scale, ws, counters, max_dec, c, g0);
+  else if (c < g0 + g1)
+    ext_tc_body(kl, vl, step, q, out, tables, tstride, hq, HKV, scale * kLog2e, c - g0, g1);
+  else
+    griddep_wait();
+}
+
 // ================================================================ generic
 // Warp per (row, q head); exact two-pass softmax in fp32 (model.py:154-159).
 template <typename T>
@@ -663,6 +708,69 @@ int32_t launch_tiles(const int32_t* step, int list, const void* q, void* out, co
   return check_launch("attn_tiles");
 }
 
+bool ext_tc_shape(int hq, int hkv, int head_dim) {
+  return head_dim == tc::D && hkv > 0 && hq == tc::GRP * hkv;
+}
+
+int32_t launch_ext_tc(const int32_t* step, const void* q, void* out, const void* kl, const void* vl,
+                      const int32_t* tables, int64_t tstride, int hq, int hkv, float scale,
+                      int n_ctas, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_ext_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM);
+    attr = true;
+  }
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_ctas);
+  cfg.blockDim = dim3(tc::THREADS);
+  cfg.dynamicSmemBytes = tc::SMEM;
+  cfg.stream = st;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_ext_tc_kernel, (const __nv_bfloat16*)kl,
+                                           (const __nv_bfloat16*)vl, step, (const __nv_bfloat16*)q,
+                                           (__nv_bfloat16*)out, tables, tstride, hq, hkv, scale * kLog2e);
+  if (e != cudaSuccess) {
+    set_last_error("attn_ext_tc launch: %s", cudaGetErrorString(e));
+    return TIM_CUDA_ERROR;
+  }
+  return check_launch("attn_ext_tc");
+}
+
+template <int D, int HKV>
+int32_t launch_step(const int32_t* step, const void* q, void* out, const void* kl, const void* vl,
+                    const int32_t* tables, int64_t tstride, int hq, float scale, float* ws, int32_t* counters,
+                    int n_ctas, int max_dec, cudaStream_t st) {
+  constexpr int SMEM = AttnCfg<D, HKV, 1>::SMEM > tc::SMEM ? AttnCfg<D, HKV, 1>::SMEM : tc::SMEM;
+  auto kern = attn_step_kernel<D, HKV>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_ctas);
+  cfg.blockDim = dim3(AttnCfg<D, HKV, 1>::THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = st;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, step, (const __nv_bfloat16*)q, (__nv_bfloat16*)out,
+                                           (const __nv_bfloat16*)kl, (const __nv_bfloat16*)vl, tables, tstride,
+                                           hq, scale, ws, counters, max_dec);
+  if (e != cudaSuccess) {
+    set_last_error("attn_step launch: %s", cudaGetErrorString(e));
+    return TIM_CUDA_ERROR;
+  }
+  return check_launch("attn_step");
+}
+
 // kv heads per CTA for multi-token tiles (the rest of the 8 warps share a head)
 constexpr int ext_hg(int hkv) { return hkv >= 8 ? 4 : (hkv >= 4 ? 2 : 1); }
 
@@ -740,7 +848,16 @@ extern "C" int32_t tim_attn_decode(const int32_t* step, int32_t mode, const void
                                                             block_tables, table_stride, hq,    \
                                                             scale, ws, counters, n_ctas, max_dec, st); \
   }
-  if (mode == 1 && ext_tc_shape(hq, hkv, head_dim))   // multi-token tiles on tcgen05 (attention_tc.cu)
+  if (mode == 2) {   // the step's decode tiles and multi-token items in one launch
+    if (head_dim == 128 && hkv == 8 && ext_tc_shape(hq, hkv, head_dim))
+      return launch_step<128, 8>(step, q, out, k_layer, v_layer, block_tables, table_stride, hq, scale, ws,
+                                 counters, n_ctas, max_dec, st);
+    const int32_t e0 = tim_attn_decode(step, 0, q, out, k_layer, v_layer, block_tables, table_stride, hq,
+                                       hkv, head_dim, scale, ws, counters, n_ctas, max_dec, dtype, stream);
+    if (e0 != TIM_OK) return e0;
+    mode = 1;
+  }
+  if (mode == 1 && ext_tc_shape(hq, hkv, head_dim))   // multi-token tiles on tcgen05 (attention_tc.cuh)
     return launch_ext_tc(step, q, out, k_layer, v_layer, block_tables, table_stride, hq, hkv, scale,
                          n_ctas, st);
   TIM_TILES(128, 8) TIM_TILES(128, 4) TIM_TILES(128, 2) TIM_TILES(128, 1)
@@ -759,6 +876,12 @@ extern "C" int32_t tim_attn_extend(const int32_t* step, int32_t max_items, const
   if (max_items <= 0) return TIM_OK;
   return launch_generic(step, max_items, q, out, k_layer, v_layer, block_tables, table_stride, hq,
                         hkv, head_dim, scale, dtype, (cudaStream_t)stream);
+}
+
+extern "C" int32_t tim_tc_trace(void* buf) {
+  unsigned long long* p = (unsigned long long*)buf;
+  if (cudaMemcpyToSymbol(tim::g_tc_trace, &p, sizeof(p)) != cudaSuccess) return TIM_CUDA_ERROR;
+  return TIM_OK;
 }
 
 extern "C" int32_t tim_set_trace(void* buf) {

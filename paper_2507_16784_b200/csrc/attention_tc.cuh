@@ -1,3 +1,6 @@
+// Included by attention.cu (one translation unit, so the single-launch step
+// kernel can host both bodies).
+#pragma once
 // K2 on the 5th-gen tensor cores: attention of the multi-token rows of a step
 // (re-encoded suffixes after a prune, tool responses, prefills) over their
 // paged prefix + causal new block (model.py:139-159).
@@ -108,7 +111,7 @@ TIM_DEV uint32_t swz(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) 
 using namespace tc;
 
 // Diagnostics: per-block %globaltimer stamps of CTA 0 (tim_tc_trace).
-__device__ unsigned long long* g_tc_trace = nullptr;
+static __device__ unsigned long long* g_tc_trace = nullptr;
 TIM_DEV unsigned long long tc_now() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -116,12 +119,12 @@ TIM_DEV unsigned long long tc_now() {
 }
 #define TCT(slot, g) do { if (tr && (g) < 64) tr[(g) * 8 + (slot)] = tc_now(); } while (0)
 
-__global__ void __launch_bounds__(tc::THREADS, 1)
-    attn_ext_tc_kernel(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat16* __restrict__ vl,
-                       const int32_t* __restrict__ step, const __nv_bfloat16* __restrict__ q,
-                       __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ tables,
-                       int64_t tstride, int hq, int hkv, float scale_log2) {
-  griddep_launch();
+// Body of the multi-token kernel for CTA `cta` of `grid` CTAs working the
+// step's ext list (warps >= 6 of a wider CTA only take part in the barriers).
+TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat16* __restrict__ vl,
+                         const int32_t* __restrict__ step, const __nv_bfloat16* __restrict__ q,
+                         __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ tables,
+                         int64_t tstride, int hq, int hkv, float scale_log2, int cta, int grid) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -135,10 +138,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   uint64_t* q_ready = pv_done + 2;     // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_ready + 2);
 
-  unsigned long long* tr = blockIdx.x == 0 ? g_tc_trace : nullptr;
+  unsigned long long* tr = cta == 0 ? g_tc_trace : nullptr;
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
   const int n_items = hd.n_ext;
-  if (n_items == 0 || (int)blockIdx.x >= n_items) {
+  if (n_items == 0 || cta >= n_items) {
     griddep_wait();   // completion of this grid must imply the preceding one's
     return;
   }
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     bool waited = false;
     int gb = 0;
     const int ch = lane & 15, tsub = lane >> 4;     // 16-byte chunk of a row, token parity
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = cta; it < n_items; it += grid) {
       const int32_t* rec = items + (int64_t)it * TIM_EXT_FIELDS;
       const int slot = rec[1], kv_len = rec[2], fresh = rec[4], head = rec[5];
       const int32_t* trow = tables + (int64_t)slot * tstride;
@@ -229,8 +232,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       auto nblk_of = [&](int it) {
         return it < n_items ? (items[(int64_t)it * TIM_EXT_FIELDS + 2] + BN - 1) / BN : 0;
       };
-      int s_it = blockIdx.x, s_j = 0, s_g = 0, s_ii = 0, s_nb = nblk_of(s_it);
-      int p_it = blockIdx.x, p_j = 0, p_g = 0, p_nb = s_nb;
+      int s_it = cta, s_j = 0, s_g = 0, s_ii = 0, s_nb = nblk_of(s_it);
+      int p_it = cta, p_j = 0, p_g = 0, p_nb = s_nb;
       bool q_ok = false;
       while (p_it < n_items) {
         bool progress = false;
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             ++s_g;
             if (++s_j == s_nb) {
               s_j = 0;
-              s_it += gridDim.x;
+              s_it += grid;
               ++s_ii;
               q_ok = false;
               s_nb = nblk_of(s_it);
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           ++p_g;
           if (++p_j == p_nb) {
             p_j = 0;
-            p_it += gridDim.x;
+            p_it += grid;
             p_nb = nblk_of(p_it);
           }
           progress = true;
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         if (!progress) __nanosleep(20);
       }
     }
-  } else {
+  } else if (warp < 4) {
     // ---------------------------------------------------------- softmax
     const int t = threadIdx.x;                       // MMA row / TMEM lane
     const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
@@ -306,9 +309,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&q_ready[qb]))
                    : "memory");
     };
-    load_q(blockIdx.x, 0);
+    load_q(cta, 0);
     int gb = 0, ii = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++ii) {
+    for (int it = cta; it < n_items; it += grid, ++ii) {
       const int32_t* rec = items + (int64_t)it * TIM_EXT_FIELDS;
       const int row0 = rec[0], kv_len = rec[2], nq = rec[3], head = rec[5];
       const int nblk = (kv_len + BN - 1) / BN;
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       const int lim = kv_len - nq + qi;              // last key this query sees (model.py:139-140)
       const int64_t qoff = ((int64_t)(row0 + qi) * hq + head * GRP + hj) * D;
       // the other Q buffer's last reader (item ii-1) has completed: prefetch
-      if (it + (int)gridDim.x < n_items) load_q(it + gridDim.x, (ii + 1) & 1);
+      if (it + (int)grid < n_items) load_q(it + grid, (ii + 1) & 1);
 
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < nblk; ++j, ++gb) {
@@ -428,49 +431,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS)
                  : "memory");
   }
-}
-
-}  // namespace tim
-
-extern "C" int32_t tim_tc_trace(void* buf) {
-  unsigned long long* p = (unsigned long long*)buf;
-  if (cudaMemcpyToSymbol(tim::g_tc_trace, &p, sizeof(p)) != cudaSuccess) return TIM_CUDA_ERROR;
-  return TIM_OK;
-}
-
-namespace tim {
-
-bool ext_tc_shape(int hq, int hkv, int head_dim) {
-  return head_dim == D && hkv > 0 && hq == GRP * hkv;
-}
-
-int32_t launch_ext_tc(const int32_t* step, const void* q, void* out, const void* kl, const void* vl,
-                      const int32_t* tables, int64_t tstride, int hq, int hkv, float scale,
-                      int n_ctas, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_ext_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    attr = true;
-  }
-  cudaLaunchAttribute attrs[1];
-  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attrs[0].val.programmaticStreamSerializationAllowed = 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_ctas);
-  cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM;
-  cfg.stream = st;
-  cfg.attrs = attrs;
-  cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_ext_tc_kernel, (const __nv_bfloat16*)kl,
-                                           (const __nv_bfloat16*)vl, step, (const __nv_bfloat16*)q,
-                                           (__nv_bfloat16*)out, tables, tstride, hq, hkv,
-                                           scale * 1.4426950408889634f);
-  if (e != cudaSuccess) {
-    set_last_error("attn_ext_tc launch: %s", cudaGetErrorString(e));
-    return TIM_CUDA_ERROR;
-  }
-  return check_launch("attn_ext_tc");
 }
 
 }  // namespace tim

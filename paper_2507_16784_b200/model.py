@@ -262,6 +262,7 @@ class StepRuntime:
         if b is not None:
             sd.rows_pad = b
             sd.last_pad = self.max_slots
+        sd.ctas = self.sms
         arr = sd.pack()
         self._ensure_rows(max(sd.rows_pad or sd.n_rows, 1))
         if self.gstep is None or self.gstep.numel() < arr.size:
@@ -463,6 +464,7 @@ class B200Transformer:
         sd.n_rows = n
         self.plan_attention(sd, rt.scratch_slot, m, n, 0)
         sd.last.append(n - 1)
+        sd.ctas = rt.sms
         step = rt.upload(sd.pack())
         self.forward_rows(rt, step, sd)
         table.append(new_pages)
@@ -567,12 +569,13 @@ class B200Transformer:
         if timed is not None:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
-        n = 0
-        for mode in ((0, 1) if has_ext else (0,)):
-            L.call("tim_attn_decode", sp, mode, rt.q.data_ptr(), rt.ctx.data_ptr(), kl, vl,
-                   rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, rt.ws.data_ptr(),
-                   rt.counters.data_ptr(), rt.n_ctas, rt.max_dec, td, st)
-            n += 1
+        # mode 2: decode tiles and multi-token items in one launch, CTAs split
+        # per the descriptor's cost model (falls back to two launches when the
+        # shape has no tcgen05 multi-token kernel)
+        L.call("tim_attn_decode", sp, 2 if has_ext else 0, rt.q.data_ptr(), rt.ctx.data_ptr(), kl, vl,
+               rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, rt.ws.data_ptr(),
+               rt.counters.data_ptr(), rt.n_ctas, rt.max_dec, td, st)
+        n = 1 if has_ext and self.ext_q else (2 if has_ext else 1)
         if timed is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()

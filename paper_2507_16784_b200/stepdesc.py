@@ -14,6 +14,7 @@ _HDR = [
     "n_rows", "n_rows_pad", "n_new", "n_segs", "n_dec", "n_ext", "n_jobs", "n_ops", "n_phases",
     "n_last", "dec_total", "off_new", "off_segs", "off_dec", "off_dec_prefix", "off_ext", "off_jobs",
     "off_spans", "off_ops", "off_phases", "off_last", "ext_total", "off_ext_prefix",
+    "split_dec_ctas", "split_ext_ctas",
 ]
 
 
@@ -21,7 +22,7 @@ class StepDesc:
     """Accumulates one step's records and packs them into an int32 array."""
 
     __slots__ = ("new", "segs", "dec", "ext", "jobs", "spans", "ops", "phase_starts", "last",
-                 "n_rows", "_last_kind", "offsets", "rows_pad", "last_pad")
+                 "n_rows", "_last_kind", "offsets", "rows_pad", "last_pad", "ctas")
 
     def __init__(self):
         self.new: list = []      # (slot, logical_idx, token, row, live_idx)
@@ -38,6 +39,7 @@ class StepDesc:
         self.offsets: dict = {}
         self.rows_pad: int | None = None   # row buffers padded to this many rows (graph bucket)
         self.last_pad = 0                  # `last` padded to this many entries (graph bucket)
+        self.ctas = 0                      # SMs of the one-launch attention (mode 2 split)
 
     # ------------------------------------------------------------- page ops
     def op(self, kind: int, slot: int, table_off: int, count: int, sp_before: int,
@@ -54,6 +56,33 @@ class StepDesc:
         for a, b in spans:
             self.spans.extend((a, b))
         self.jobs.append((slot, old_len, s, reencode_from, off, len(spans), out_row, keep))
+
+    # Cost model of the one-launch attention (mode 2), in SM-microseconds
+    # measured on B200: a decode-tile CTA streams ~44 KB/us of page rows; a
+    # multi-token item costs ~2 us plus ~0.95 us per 64-key block.
+    DEC_US_PER_TOKEN = 4096 / 44e3
+    EXT_US_PER_BLOCK = 0.95
+    EXT_US_PER_ITEM = 2.0
+
+    def attention_split(self) -> tuple[int, int]:
+        """CTAs given to the decode tiles and to the multi-token items when
+        both run in one launch: minimise the slower side's estimated time."""
+        G = self.ctas
+        if G <= 0 or not self.ext:
+            return (G, 0)
+        if not self.dec:
+            return (0, G)
+        w0 = sum(d[2] for d in self.dec) * self.DEC_US_PER_TOKEN
+        times = sorted((self.EXT_US_PER_ITEM + self.EXT_US_PER_BLOCK * ((e[2] + 63) // 64)
+                        for e in self.ext), reverse=True)
+        n = len(times)
+        best, best_g1 = None, 1
+        for g1 in range(1, min(G - 1, n) + 1):
+            t1 = sum(times[0::g1])          # CTA 0's items (longest first, round-robin)
+            t = max(w0 / (G - g1), t1)
+            if best is None or t < best:
+                best, best_g1 = t, g1
+        return (G - best_g1, best_g1)
 
     # ---------------------------------------------------------------- pack
     def pack(self) -> np.ndarray:
@@ -108,6 +137,7 @@ class StepDesc:
             n_jobs=len(self.jobs), n_ops=len(self.ops), n_phases=len(self.phase_starts),
             n_last=len(last), dec_total=int(prefix[-1]), ext_total=int(eprefix[-1]),
         )
+        hdr["split_dec_ctas"], hdr["split_ext_ctas"] = self.attention_split()
         self.offsets = hdr
         head = np.zeros(L.HEADER_INTS, dtype=np.int32)
         for i, k in enumerate(_HDR):

@@ -107,9 +107,10 @@ def _extend_case(hq, hkv, d, dtype, segs_mn, seed):
     return kp, vp, tab, stride, q, sd, rows
 
 
+@pytest.mark.parametrize("one_launch", [False, True])
 @pytest.mark.parametrize("n_ctas", [None, 5])
 @pytest.mark.parametrize("hq,hkv", [(32, 8), (16, 4), (4, 4), (32, 2)])
-def test_extend_tiles_bf16_matches_oracle(hq, hkv, n_ctas):
+def test_extend_tiles_bf16_matches_oracle(hq, hkv, n_ctas, one_launch):
     """Multi-query tiles (re-encode / prefill / tool rows) through the unified
     split-K kernel: paged prefix fully visible + causal new block."""
     d = 128
@@ -127,14 +128,15 @@ def test_extend_tiles_bf16_matches_oracle(hq, hkv, n_ctas):
             for gi in range(ngr):
                 sd.ext.append((row + q0, i, m + q0 + nq, nq, m, gi))
         row += n
+    ctas = n_ctas or L.load().tim_sm_count()
+    sd.ctas = ctas
     step = _dev(sd.pack())
     out = torch.zeros(rows, hq, d, device="cuda", dtype=torch.bfloat16)
-    ctas = n_ctas or L.load().tim_sm_count()
     ntiles = len(sd.dec) + len(sd.ext)
     ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, ntiles, hkv, d), device="cuda")
     cnt = torch.zeros(ntiles * 8, device="cuda", dtype=torch.int32)
     tab_d = _dev(tab)
-    for mode in (0, 1):
+    for mode in ((2,) if one_launch else (0, 1)):
         L.call("tim_attn_decode", _ptr(step), mode, _ptr(q), _ptr(out), _ptr(kp), _ptr(vp),
                _ptr(tab_d), stride, hq, hkv, d, 1.0 / np.sqrt(d), _ptr(ws), _ptr(cnt), ctas,
                ntiles, L.DTYPE_BF16, _stream())

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--dump", action="store_true")
+    ap.add_argument("--isolated", action="store_true",
+                    help="CUDA events around every launch (as bench.py times layer 0): no PDL overlap")
     a = ap.parse_args()
     hq, hkv, d = 32, 8, 128
     rng = np.random.default_rng(0)
@@ -65,7 +67,17 @@ def main():
     # back-to-back launches over rotating layers (inputs > L2), so host launch
     # latency is hidden behind the previous kernel and events time the GPU only
     times = []
-    for it in range(a.iters):
+    if a.isolated:
+        for it in range(a.iters):
+            for l in range(a.layers):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                run(l)
+                e1.record()
+                times.append((e0, e1))
+        torch.cuda.synchronize()
+        times = [x.elapsed_time(y) for x, y in times]
+    for it in range(0 if a.isolated else a.iters):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for l in range(a.layers):

@@ -49,7 +49,7 @@ def main():
     res = {}
     qpi = L.load().tim_extend_queries_per_item(hq, hkv, d, L.DTYPE_BF16)
     ngroups = L.load().tim_extend_head_groups(hq, hkv, d)
-    for variant, (qpt, ngr) in {"mode0": (4, 1), "mode1": (qpi, ngroups)}.items():
+    for variant, (qpt, ngr) in {"mode0": (4, 1), "mode1": (qpi, ngroups), "mode2": (qpi, ngroups)}.items():
         if a.only and variant != a.only:
             continue
         sd = StepDesc()
@@ -65,12 +65,19 @@ def main():
                     for g in range(ngr):
                         sd.ext.append((row + q0, i, m + q0 + nq, nq, m, g))
             row += n
+        sd.ctas = ctas
         step = torch.from_numpy(sd.pack()).cuda()
+        split = (sd.offsets["split_dec_ctas"], sd.offsets["split_ext_ctas"])
         maxd = max(len(sd.dec), len(sd.ext)) + 8
         ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, maxd, hkv, d), device="cuda")
         cnt = torch.zeros(maxd * 8, dtype=torch.int32, device="cuda")
 
         def run(l):
+            if variant == "mode2":
+                L.call("tim_attn_decode", step.data_ptr(), 2, q.data_ptr(), out.data_ptr(), K[l].data_ptr(),
+                       V[l].data_ptr(), tab_d.data_ptr(), stride, hq, hkv, d, 1 / np.sqrt(d), ws.data_ptr(),
+                       cnt.data_ptr(), ctas, maxd, L.DTYPE_BF16, st)
+                return
             L.call("tim_attn_decode", step.data_ptr(), 0, q.data_ptr(), out.data_ptr(), K[l].data_ptr(),
                    V[l].data_ptr(), tab_d.data_ptr(), stride, hq, hkv, d, 1 / np.sqrt(d), ws.data_ptr(),
                    cnt.data_ptr(), ctas, maxd, L.DTYPE_BF16, st)
@@ -106,12 +113,13 @@ def main():
                 if t[g, 0] == 0:
                     break
                 print(g, " ".join(f"{n}={(t[g, i] - t0) / 1000:7.2f}" for i, n in enumerate(names)), file=sys.stderr)
-        res[variant] = {"us": round(us, 1), "gbs": round(ub / us / 1e3), "tiles": len(sd.dec) + len(sd.ext),
+        res[variant] = {"us": round(us, 1), "split": split, "gbs": round(ub / us / 1e3), "tiles": len(sd.dec) + len(sd.ext),
                         "streamed_tokens": int(sum(t[2] for t in sd.dec) + sum(t[2] for t in sd.ext) / ngr)}
         res.setdefault("_outs", []).append(ref)
     outs = res.pop("_outs")
-    if len(outs) == 2:
+    if len(outs) == 3:
         res["maxdiff_mode1_vs_0"] = float((outs[1] - outs[0]).abs().max())
+        res["maxdiff_mode2_vs_0"] = float((outs[2] - outs[0]).abs().max())
     res["unique_MB"] = round(ub / 1e6, 1)
     print(json.dumps(res))
 

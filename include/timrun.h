@@ -147,19 +147,24 @@ int32_t tim_rope_kv_store(const void* qkv, const void* h, int32_t dm, float eps,
 int32_t tim_silu_rms(void* u, int32_t n_rows, int32_t width, const void* h, int32_t dm, float eps,
                      int32_t dtype, void* stream);
 
-/* K1+K6: split-K (stream-K) paged GQA attention over retained pages only
- * (model.py:149-159).  Work items are query tiles {row, slot, kv_len, nq, m,
- * group}: nq consecutive query rows of one request; query i of a tile sees
- * keys [0, kv_len - nq + i] (prefix fully visible, causal inside the new
- * block); keys >= m were written by this step.  mode 0 runs the step's decode
- * tiles (`dec`: one query x all kv heads, whole page rows); mode 1 runs its
- * multi-token tiles (`ext`: tim_extend_queries_per_item queries x one of
- * tim_extend_head_groups kv-head groups), so re-encode / prefill / tool rows
- * share one K/V stream per tile.  The kernel is launched with programmatic
- * dependent launch and streams older pages before the preceding RoPE+store
- * kernel finishes.  `n_ctas` persistent CTAs split the concatenated key ranges
- * of all tiles evenly; tiles spanning several CTAs are merged in-kernel by the
- * last CTA to finish (log-sum-exp combine).
+/* K1+K2+K6: paged GQA attention over retained pages only (model.py:149-159),
+ * replacing the per-request attention loop of TinyTransformer._forward
+ * (model.py:142-161) called from Engine._advance (scheduler.py:372).  Work
+ * items are query tiles {row, slot, kv_len, nq, m, group}: nq consecutive
+ * query rows of one request; query i of a tile sees keys [0, kv_len - nq + i]
+ * (prefix fully visible, causal inside the new block); keys >= m were written
+ * by this step.
+ *   mode 0: the step's decode tiles (`dec`: tile_q queries x all kv heads,
+ *           whole page rows), split-K over `n_ctas` persistent CTAs (stream-K);
+ *           tiles spanning several CTAs are merged in-kernel (log-sum-exp).
+ *   mode 1: the multi-token items (`ext`: tim_extend_queries_per_item queries
+ *           x one of tim_extend_head_groups kv-head groups); on the tcgen05
+ *           shape (D = 128, Hq = 4 Hkv) one item = 128 MMA rows in TMEM.
+ *   mode 2: both lists in ONE launch, CTAs split per the descriptor's
+ *           split_dec_ctas / split_ext_ctas (two launches where no tcgen05
+ *           kernel exists for the shape).
+ * Launched with programmatic dependent launch; older pages stream before the
+ * preceding RoPE+store kernel finishes.
  * ws: float workspace of tim_decode_ws_floats(n_ctas, max_dec, hkv, D) floats;
  * counters: int32[max_dec * 8] zero-initialised once (self-resetting); max_dec
  * bounds the tile count. */
@@ -177,6 +182,10 @@ int32_t tim_extend_head_groups(int32_t hq, int32_t hkv, int32_t head_dim);
  * buf[4*cta .. 4*cta+3] = {start, first stage landed, main loop end, end};
  * pass NULL to disable. */
 int32_t tim_set_trace(void* buf);
+/* Diagnostics: an empty grid launched like the attention kernel (n_ctas x
+ * threads, smem dynamic bytes, programmatic launch): the fixed cost that
+ * CUDA-event bracketing of one launch measures. */
+int32_t tim_noop(int32_t n_ctas, int32_t threads, int32_t smem, void* stream);
 /* Diagnostics: per-64-key-block %globaltimer stamps of CTA 0 of the tcgen05
  * multi-token kernel, buf[8*block + {0..5}]; NULL disables. */
 int32_t tim_tc_trace(void* buf);

@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(NT)
   constexpr int V = Vec<T>::V;
   constexpr int MAXH = 4;
   griddep_launch();   // the attention kernel may start streaming old pages now
+  griddep_wait();     // qkv / h come from the preceding GEMM (programmatic launch)
   const int r = blockIdx.x;
   const int half = D >> 1;
   const int gph = half / V;                       // rope vector groups per head
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(NT)
   constexpr int V = Vec<T>::V;
   constexpr int MAXH = 4;
   griddep_launch();   // the down-projection GEMM may start streaming its weights
+  griddep_wait();     // u / h come from the preceding GEMM (programmatic launch)
   const int r = blockIdx.x;
   T* row = u + (int64_t)r * width;
   const T* hr = h ? h + (int64_t)r * dm : nullptr;
@@ -293,6 +295,23 @@ __global__ void argmax_kernel(const T* __restrict__ logits, int n_rows, int voca
 
 using namespace tim;
 
+// Launch with programmatic stream serialization: the grid may be scheduled
+// while the preceding kernel drains; the kernels above wait (griddepcontrol)
+// before touching its outputs.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t st, Args... args) {
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = st;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 #define TIM_DISPATCH(dtype, ...)                                   \
   do {                                                             \
     if ((dtype) == TIM_DTYPE_F32) {                                \
@@ -319,9 +338,9 @@ extern "C" int32_t tim_rope_kv_store(const void* qkv, const void* h, int32_t dm,
     set_last_error("rope_kv_store: head_dim must be a multiple of %d and dm of %d", 2 * V, V);
     return TIM_BAD_ARGUMENT;
   }
-  TIM_DISPATCH(dtype, rope_kv_kernel<T, 256, 2><<<n_rows, 256, 0, (cudaStream_t)stream>>>(
-                          (const T*)qkv, (const T*)h, dm, eps, row_pos, row_pages, cos_tab, sin_tab,
-                          hq, hkv, head_dim, (T*)q_out, (T*)k_layer, (T*)v_layer));
+  TIM_DISPATCH(dtype, launch_pdl(rope_kv_kernel<T, 256, 2>, n_rows, 256, (cudaStream_t)stream,
+                                 (const T*)qkv, (const T*)h, dm, eps, row_pos, row_pages, cos_tab,
+                                 sin_tab, hq, hkv, head_dim, (T*)q_out, (T*)k_layer, (T*)v_layer));
   return check_launch("rope_kv_store");
 }
 
@@ -333,8 +352,8 @@ extern "C" int32_t tim_silu_rms(void* u, int32_t n_rows, int32_t width, const vo
     set_last_error("silu_rms: width and dm must be multiples of %d", V);
     return TIM_BAD_ARGUMENT;
   }
-  TIM_DISPATCH(dtype, silu_rms_kernel<T, 256, 6><<<n_rows, 256, 0, (cudaStream_t)stream>>>(
-                          (T*)u, width, (const T*)h, dm, eps));
+  TIM_DISPATCH(dtype, launch_pdl(silu_rms_kernel<T, 256, 6>, n_rows, 256, (cudaStream_t)stream, (T*)u,
+                                 width, (const T*)h, dm, eps));
   return check_launch("silu_rms");
 }
 

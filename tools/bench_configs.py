@@ -86,11 +86,14 @@ def run_c4(a):
     model = tr.B200Transformer(cfg)
     n = 32
     eng = tr.Engine(model, tr.BatchConfig(max_batch=n, buffer_threshold=2, position_limit=16384,
-                                          pool_pages=n * 2048, max_queue=64, check_masks=False,
+                                          pool_pages=n * (a.prompt + 2048), max_queue=64, check_masks=False,
                                           max_output_tokens=140_000))
+    # a fixed prompt (never pruned) loads the retained working
+    # memory near the position cap, as SURVEY §8d suggests for C4
+    prompt = "a" * a.prompt
     for i in range(n):
         t = make_trace_from_text(deep_recursion_doc(8, 3, seed=i, text_chars=16))
-        eng.submit(f"g{i}:", script=t.script)
+        eng.submit(prompt + f"g{i}:", script=t.script)
     eng.runtime.precapture()
     t0 = time.perf_counter()
     for _ in range(a.skip):
@@ -98,7 +101,7 @@ def run_c4(a):
     w = timed_window(eng, a.steps)
     reqs = list(eng.requests.values())
     return {"config": "C4 long horizon: 32 x deep_recursion(8 levels, 3-way, 16-char texts) "
-                      "= 134,480 generated tokens each, T=2, position limit 16384",
+                      f"= 134,480 generated tokens each, {a.prompt}-token prompt, T=2, position limit 16384",
             "skip_steps": a.skip, "steps": a.steps, "tokens_per_s": w["tokens"] / (w["ms"] * 1e-3),
             "ms_per_step": w["ms"] / a.steps,
             "pages_freed_per_s": w["pages_freed"] / (w["ms"] * 1e-3),
@@ -137,5 +140,6 @@ if __name__ == "__main__":
     ap.add_argument("--config", required=True, choices=["c1", "c4", "c5"])
     ap.add_argument("--skip", type=int, default=600)
     ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--prompt", type=int, default=12000, help="C4 prompt tokens")
     a = ap.parse_args()
     print(json.dumps({"c1": run_c1, "c4": run_c4, "c5": run_c5}[a.config](a)))

@@ -69,7 +69,8 @@ typedef struct {
   int32_t off_ops, off_phases, off_last;
   int32_t ext_total, off_ext_prefix;
   int32_t split_dec_ctas, split_ext_ctas;  /* mode-2 attention: CTAs on dec tiles / ext items */
-  int32_t reserved[7];
+  int32_t serial;                          /* step serial (!= 0) matching tim_attn_plan's record */
+  int32_t reserved[6];
 } tim_step_header;  /* 32 int32 */
 
 #define TIM_NEW_FIELDS 5
@@ -174,6 +175,12 @@ int32_t tim_attn_decode(const int32_t* step, int32_t mode, const void* q, void* 
                         int64_t table_stride, int32_t hq, int32_t hkv, int32_t head_dim,
                         float scale, float* ws, int32_t* counters, int32_t n_ctas, int32_t max_dec,
                         int32_t dtype, void* stream);
+/* Per-step plan of the decode-tile partition (each K1 CTA's first tile),
+ * written into the tail of `ws` once per step (the partition is the same for
+ * every layer); K1 uses it when the descriptor's serial matches, else it
+ * searches itself.  n_ctas / max_dec / head_dim as passed to tim_attn_decode. */
+int32_t tim_attn_plan(const int32_t* step, int32_t n_ctas, int32_t max_dec, int32_t head_dim, float* ws,
+                      void* stream);
 /* Queries per multi-token tile and kv-head groups per query for a config. */
 int32_t tim_extend_queries_per_item(int32_t hq, int32_t hkv, int32_t head_dim, int32_t dtype);
 int32_t tim_extend_head_groups(int32_t hq, int32_t hkv, int32_t head_dim);

@@ -159,6 +159,7 @@ class StepRuntime:
         self.step_dev = None
         self.step_host = None
         self.sms = L.load().tim_sm_count()
+        self.serial = 0              # step serial stamped into descriptors (attention plan)
         self.last_tokens = None
         self.last_logits = None
         self.launches = 0
@@ -263,6 +264,8 @@ class StepRuntime:
             sd.rows_pad = b
             sd.last_pad = self.max_slots
         sd.ctas = self.sms
+        self.serial = (self.serial % 0x7FFFFFFF) + 1
+        sd.serial = self.serial
         arr = sd.pack()
         self._ensure_rows(max(sd.rows_pad or sd.n_rows, 1))
         if self.gstep is None or self.gstep.numel() < arr.size:
@@ -401,9 +404,15 @@ class B200Transformer:
                box_rows, 64)
         return buf
 
+    # Diagnostics only (bench ablation of kernel classes; results are garbage):
+    # TIMRUN_DIAG_SKIP=gemm,rope,silu,attn drops those launches from the step.
+    _DIAG_SKIP = frozenset(x for x in os.environ.get("TIMRUN_DIAG_SKIP", "").split(",") if x)
+
     def _gemm(self, rt, li: int, which: int, x, y, res, T: int) -> int:
         """y (+)= x @ W for projection `which` (0 qkv, 1 o, 2 up, 3 down):
         the weight-streaming kernel for <= 64 rows, cuBLAS otherwise."""
+        if "gemm" in self._DIAG_SKIP:
+            return 0
         wt = (self.wqkv_t, self.wo_t, self.w1_t, self.w2_t)[which][li]
         if self.skinny and T <= 64:
             N, K = wt.shape
@@ -465,6 +474,8 @@ class B200Transformer:
         self.plan_attention(sd, rt.scratch_slot, m, n, 0)
         sd.last.append(n - 1)
         sd.ctas = rt.sms
+        rt.serial = (rt.serial % 0x7FFFFFFF) + 1
+        sd.serial = rt.serial
         step = rt.upload(sd.pack())
         self.forward_rows(rt, step, sd)
         table.append(new_pages)
@@ -539,14 +550,18 @@ class B200Transformer:
         cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
         dm = cfg.model_dim
         h = rt.h[:T]
+        if self.tensor_cores:   # decode-tile partition of this step, shared by all layers
+            L.call("tim_attn_plan", sp, rt.n_ctas, rt.max_dec, cfg.head_dim, rt.ws.data_ptr(), st)
         L.call("tim_embed", rt.row_tokens.data_ptr(), T, self.emb.data_ptr(), dm, h.data_ptr(), td, st)
-        return 1 + self._layer_head(rt, 0, T)
+        return (2 if self.tensor_cores else 1) + self._layer_head(rt, 0, T)
 
     def _layer_head(self, rt, li, T) -> int:
         """QKV GEMM on the raw residual + fused RMSNorm-scale/RoPE/page store."""
         cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
         dm, D = cfg.model_dim, cfg.head_dim
         n = self._gemm(rt, li, 0, rt.h, rt.qkv, None, T)
+        if "rope" in self._DIAG_SKIP:
+            return n
         L.call("tim_rope_kv_store", rt.qkv.data_ptr(), rt.h.data_ptr(), dm, 1e-6, T,
                rt.row_pos.data_ptr(), rt.row_pages.data_ptr(), self.cos.data_ptr(),
                self.sin.data_ptr(), cfg.heads, cfg.n_kv, D, rt.q.data_ptr(),
@@ -572,6 +587,8 @@ class B200Transformer:
         # mode 2: decode tiles and multi-token items in one launch, CTAs split
         # per the descriptor's cost model (falls back to two launches when the
         # shape has no tcgen05 multi-token kernel)
+        if "attn" in self._DIAG_SKIP:
+            return 0
         L.call("tim_attn_decode", sp, 2 if has_ext else 0, rt.q.data_ptr(), rt.ctx.data_ptr(), kl, vl,
                rt.tables.data_ptr(), tstride, hq, hkv, D, self.scale, rt.ws.data_ptr(),
                rt.counters.data_ptr(), rt.n_ctas, rt.max_dec, td, st)
@@ -588,7 +605,8 @@ class B200Transformer:
         dm = cfg.model_dim
         n = self._gemm(rt, li, 1, rt.ctx, rt.h, rt.h, T)
         n += self._gemm(rt, li, 2, rt.h, rt.u, None, T)
-        L.call("tim_silu_rms", rt.u.data_ptr(), T, cfg.n_mlp, rt.h.data_ptr(), dm, 1e-6, td, st)
+        if "silu" not in self._DIAG_SKIP:
+            L.call("tim_silu_rms", rt.u.data_ptr(), T, cfg.n_mlp, rt.h.data_ptr(), dm, 1e-6, td, st)
         n += self._gemm(rt, li, 3, rt.u, rt.h, rt.h, T)
         return 1 + n
 

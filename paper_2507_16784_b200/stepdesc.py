@@ -14,7 +14,7 @@ _HDR = [
     "n_rows", "n_rows_pad", "n_new", "n_segs", "n_dec", "n_ext", "n_jobs", "n_ops", "n_phases",
     "n_last", "dec_total", "off_new", "off_segs", "off_dec", "off_dec_prefix", "off_ext", "off_jobs",
     "off_spans", "off_ops", "off_phases", "off_last", "ext_total", "off_ext_prefix",
-    "split_dec_ctas", "split_ext_ctas",
+    "split_dec_ctas", "split_ext_ctas", "serial",
 ]
 
 
@@ -22,7 +22,7 @@ class StepDesc:
     """Accumulates one step's records and packs them into an int32 array."""
 
     __slots__ = ("new", "segs", "dec", "ext", "jobs", "spans", "ops", "phase_starts", "last",
-                 "n_rows", "_last_kind", "offsets", "rows_pad", "last_pad", "ctas")
+                 "n_rows", "_last_kind", "offsets", "rows_pad", "last_pad", "ctas", "serial")
 
     def __init__(self):
         self.new: list = []      # (slot, logical_idx, token, row, live_idx)
@@ -40,6 +40,7 @@ class StepDesc:
         self.rows_pad: int | None = None   # row buffers padded to this many rows (graph bucket)
         self.last_pad = 0                  # `last` padded to this many entries (graph bucket)
         self.ctas = 0                      # SMs of the one-launch attention (mode 2 split)
+        self.serial = 0                    # step serial for the attention plan (0: no plan)
 
     # ------------------------------------------------------------- page ops
     def op(self, kind: int, slot: int, table_off: int, count: int, sp_before: int,
@@ -138,6 +139,7 @@ class StepDesc:
             n_last=len(last), dec_total=int(prefix[-1]), ext_total=int(eprefix[-1]),
         )
         hdr["split_dec_ctas"], hdr["split_ext_ctas"] = self.attention_split()
+        hdr["serial"] = self.serial
         self.offsets = hdr
         head = np.zeros(L.HEADER_INTS, dtype=np.int32)
         for i, k in enumerate(_HDR):

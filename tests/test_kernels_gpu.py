@@ -52,9 +52,11 @@ def _tables(lengths, cap, stride, seed):
     return tab
 
 
+@pytest.mark.parametrize("planned", [False, True])
 @pytest.mark.parametrize("n_ctas", [None, 3, 1])
 @pytest.mark.parametrize("hq,hkv", [(32, 8), (16, 4), (8, 8), (32, 2)])
-def test_decode_bf16_matches_oracle(n_ctas, hq, hkv):
+def test_decode_bf16_matches_oracle(n_ctas, hq, hkv, planned):
+    """Decode tiles (K1), with and without the per-step plan (tim_attn_plan)."""
     d = 128
     lengths = [1, 2, 15, 16, 17, 100, 777, 1500, 33, 4096]
     cap = sum(lengths) + 7
@@ -66,11 +68,14 @@ def test_decode_bf16_matches_oracle(n_ctas, hq, hkv):
     sd = StepDesc()
     for i, n in enumerate(lengths):
         sd.dec.append((i, i, n, 1, n - 1, 0))
+    sd.serial = 7 if planned else 0
     step = _dev(sd.pack())
     out = torch.zeros(len(lengths), hq, d, device="cuda", dtype=torch.bfloat16)
     sms = L.load().tim_sm_count()
     ctas = sms if n_ctas is None else n_ctas
     ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, len(lengths), hkv, d), device="cuda")
+    if planned:
+        L.call("tim_attn_plan", _ptr(step), ctas, len(lengths), d, _ptr(ws), _stream())
     cnt = torch.zeros(len(lengths) * 8, device="cuda", dtype=torch.int32)
     tab_d = _dev(tab)
     for _ in range(2):  # twice: counters must self-reset

@@ -30,7 +30,6 @@ namespace tim {
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kIdChunk = 512;       // page ids staged per producer refill (multiple of TK)
-constexpr int kFastPieces = 4;      // partials merged per round trip by K6
 constexpr int kMinTokensPerCta = 64;  // below this many kv tokens per CTA, use fewer CTAs
 
 // ===================================================================== K1
@@ -114,83 +113,13 @@ struct TileLane {
 };
 #define TIM_SHFL(v, i) __shfl_sync(0xffffffffu, (v), (i))
 
-TIM_DEV int atom_add_acq_rel(int32_t* p) {
-  int old;
-  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
-  return old;
+TIM_DEV void red_add_release(int32_t* p) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p) : "memory");
 }
-
-// K6: merge of the pieces of one (tile, consumer warp) split across CTAs:
-// out = sum_p exp2(m_p - M) O_p / sum_p exp2(m_p - M) l_p.  Rows are merged 4
-// at a time and partials kFastPieces at a time with an online (running-max)
-// merge; every load of a chunk is issued before any use.
-template <int D, int HKV, int HG, int WPH>
-TIM_DEV void merge_pieces(const float* __restrict__ ws_o, const float* __restrict__ ws_ml,
-                          __nv_bfloat16* __restrict__ out, int r, int warp, int c_first, int c_last,
-                          int qrow, int nq, int hgrp, int hq, int lane) {
-  const int grp = hq / HKV, qpw = 16 / grp;
-  const int hloc = warp / WPH, sub = warp % WPH;
-  const int kvh = hgrp * HG + hloc;
-  int nw_q = nq - sub * qpw;
-  nw_q = nw_q < 0 ? 0 : (nw_q > qpw ? qpw : nw_q);
-  const int nrows = nw_q * grp;
-  for (int r0w = 0; r0w < nrows; r0w += 4) {
-    float M[4], den[4];
-    float4 acc[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      M[k] = -INFINITY;
-      den[k] = 0.f;
-      acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    for (int cb = c_first; cb <= c_last; cb += kFastPieces) {
-      float2 ml[4][kFastPieces];
-      float4 ov[4][kFastPieces];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-#pragma unroll
-        for (int p = 0; p < kFastPieces; ++p) {
-          ml[k][p] = make_float2(-INFINITY, 0.f);
-          ov[k][p] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (r0w + k < nrows && cb + p <= c_last) {
-            const int64_t pr = ((int64_t)(cb + p + r) * 8 + warp) * 16 + r0w + k;
-            ml[k][p] = __ldcg(reinterpret_cast<const float2*>(ws_ml + pr * 2));
-            if (lane * 4 < D) ov[k][p] = __ldcg(reinterpret_cast<const float4*>(ws_o + pr * D) + lane);
-          }
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float mc = M[k];
-#pragma unroll
-        for (int p = 0; p < kFastPieces; ++p) mc = fmaxf(mc, ml[k][p].x);
-        const float sc = M[k] == -INFINITY ? 0.f : fast_exp2(M[k] - mc);
-        den[k] *= sc;
-        acc[k].x *= sc; acc[k].y *= sc; acc[k].z *= sc; acc[k].w *= sc;
-#pragma unroll
-        for (int p = 0; p < kFastPieces; ++p) {
-          const float w = ml[k][p].x == -INFINITY ? 0.f : fast_exp2(ml[k][p].x - mc);
-          den[k] += w * ml[k][p].y;
-          acc[k].x += w * ov[k][p].x; acc[k].y += w * ov[k][p].y;
-          acc[k].z += w * ov[k][p].z; acc[k].w += w * ov[k][p].w;
-        }
-        M[k] = mc;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int rr = r0w + k;
-      if (rr < nrows && lane * 4 < D) {
-        const int qi = sub * qpw + rr / grp;
-        const int64_t oidx = (int64_t)(qrow + qi) * hq + kvh * grp + (rr % grp);
-        const float inv = 1.f / den[k];
-        uint2 pk;
-        pk.x = pack_bf16(acc[k].x * inv, acc[k].y * inv);
-        pk.y = pack_bf16(acc[k].z * inv, acc[k].w * inv);
-        *reinterpret_cast<uint2*>(out + oidx * D + lane * 4) = pk;
-      }
-    }
-  }
+TIM_DEV int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // ------------------------------------------------------------- per-step plan
@@ -418,9 +347,8 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
   float* ws_o = ws;
   float* ws_ml = ws + (int64_t)(grid + max_dec) * slot_floats;
   int it = 0, rb = r0;
-  int split_first = -1, split_last = -1;   // tiles this warp left partials for
-  int old_first = 0, old_last = 0;         // their arrival counts (lane 0)
-  bool first_sent = false;
+  int pend0 = -1, pend1 = -1;   // tiles this warp left partials for
+  bool sent0 = false;           // pend0 already signalled
 
   // q fragments of a tile for this warp (the A operand of S = Q K^T).  The
   // next tile's fragments are fetched into the same registers as soon as the
@@ -567,76 +495,92 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
 
     if (trace && threadIdx.x == 0) trace[4 * blockIdx.x + 2] = gtimer();
     // ------------------------------------------------------------ epilogue
-    // Per warp, no barrier and no wait: a tile covered by one CTA is written
-    // directly; otherwise the warp stores its unnormalised partial (O, m, l
-    // per row) with fire-and-forget stores and moves on.  Only a CTA's first
-    // and last tiles can be split; their arrival counters are bumped after
-    // the stream (below), when the stores have long drained, so the ring never
-    // waits on an atomic round trip.
+    // Per warp, no CTA barrier.  A tile covered by one CTA is written
+    // directly.  A split tile is merged (K6) by its designated piece: the one
+    // in the tile's first CTA, which is always that CTA's LAST segment, so
+    // the merge never stalls a stream.  Every other piece stores its
+    // unnormalised partial (O, m, l per row) with fire-and-forget stores and
+    // later bumps the (tile, warp) counter with a release reduction; the
+    // merger waits for the count, combines the partials with its own
+    // registers (its own partial is never written) and re-arms the counter.
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 1);
       l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 2);
     }
-    if (cta_of(lo, G, N) == cta_of(hi - 1, G, N)) {
+    const int cf = (int)cta_of(lo, G, N), cl = (int)cta_of(hi - 1, G, N);
+    if (cf != cl && nrows > 0 && c != cf) {
+      // non-merger piece: park the partial, signal after the stream
+      if (pend0 < 0) pend0 = r; else pend1 = r;
+      const int64_t wslot = ((int64_t)(c + r) * 8 + warp) * 16;   // first of this warp's 16 partial rows
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
+        const int rr = g + 8 * h;
         if (valid[h]) {
-          const float inv = 1.f / l_r[h];
-          __nv_bfloat16* ob = out + (int64_t)orow[h] * D;
+          float* ob = ws_o + (wslot + rr) * D;
 #pragma unroll
           for (int j = 0; j < C::NT; ++j)
-            *reinterpret_cast<uint32_t*>(ob + j * 8 + 2 * t) =
-                pack_bf16(o[j][2 * h] * inv, o[j][2 * h + 1] * inv);
+            __stcg(reinterpret_cast<float2*>(ob + j * 8 + 2 * t), make_float2(o[j][2 * h], o[j][2 * h + 1]));
+          if (t == 0) __stcg(reinterpret_cast<float2*>(ws_ml + (wslot + rr) * 2), make_float2(m_r[h], l_r[h]));
         }
       }
       continue;
     }
-    if (nrows == 0) continue;
-    // The arrival for the CTA's first split tile goes out before the last
-    // tile's partial stores, so its release fence has nothing left to drain.
-    if (!has_next && split_first >= 0 && lane == 0) {
-      old_first = atom_add_acq_rel(counters + (int64_t)split_first * 8 + warp);
-      first_sent = true;
+    if (cf != cl && nrows > 0) {
+      // merger (this CTA's last segment).  Publish this warp's earlier piece
+      // first (its stores drained long ago), so no CTA ever waits on a CTA
+      // that is itself waiting.
+      if (pend0 >= 0 && !sent0 && lane == 0) red_add_release(counters + (int64_t)pend0 * 8 + warp);
+      sent0 = true;
+      int32_t* cnt = counters + (int64_t)r * 8 + warp;
+      if (lane == 0) {
+        while (ld_acquire(cnt) < cl - cf) {
+        }
+      }
+      __syncwarp();
+      (void)ld_acquire(cnt);   // every lane acquires the published partials
+      __syncwarp();
+      if (lane == 0) *cnt = 0;   // re-arm for the next launch
+      for (int p = cf + 1; p <= cl; ++p) {
+        const int64_t wslot = ((int64_t)(p + r) * 8 + warp) * 16;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int rr = g + 8 * h;
+          if (!valid[h]) continue;
+          const float2 ml = __ldcg(reinterpret_cast<const float2*>(ws_ml + (wslot + rr) * 2));
+          const float* ob = ws_o + (wslot + rr) * D;
+          float2 op[C::NT];
+#pragma unroll
+          for (int j = 0; j < C::NT; ++j) op[j] = __ldcg(reinterpret_cast<const float2*>(ob + j * 8 + 2 * t));
+          const float mm = fmaxf(m_r[h], ml.x);
+          const float sa = m_r[h] == -INFINITY ? 0.f : fast_exp2(m_r[h] - mm);
+          const float sb = ml.x == -INFINITY ? 0.f : fast_exp2(ml.x - mm);
+#pragma unroll
+          for (int j = 0; j < C::NT; ++j) {
+            o[j][2 * h] = o[j][2 * h] * sa + op[j].x * sb;
+            o[j][2 * h + 1] = o[j][2 * h + 1] * sa + op[j].y * sb;
+          }
+          l_r[h] = l_r[h] * sa + ml.y * sb;
+          m_r[h] = mm;
+        }
+      }
     }
-    if (r == r0) split_first = r; else split_last = r;
-    const int64_t wslot = ((int64_t)(c + r) * 8 + warp) * 16;   // first of this warp's 16 partial rows
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int rr = g + 8 * h;
       if (valid[h]) {
-        float* ob = ws_o + (wslot + rr) * D;
+        const float inv = 1.f / l_r[h];
+        __nv_bfloat16* ob = out + (int64_t)orow[h] * D;
 #pragma unroll
         for (int j = 0; j < C::NT; ++j)
-          __stcg(reinterpret_cast<float2*>(ob + j * 8 + 2 * t), make_float2(o[j][2 * h], o[j][2 * h + 1]));
-        if (t == 0) __stcg(reinterpret_cast<float2*>(ws_ml + (wslot + rr) * 2), make_float2(m_r[h], l_r[h]));
+          *reinterpret_cast<uint32_t*>(ob + j * 8 + 2 * t) =
+              pack_bf16(o[j][2 * h] * inv, o[j][2 * h + 1] * inv);
       }
     }
   }
-  // Arrivals for the split tiles (acq_rel: publishes this warp's partials and,
-  // for the last piece to arrive, acquires everyone else's); the warp that
-  // completes a (tile, warp) pair merges it (K6) and re-arms its counter.
-  // Both atomics are in flight together.
+  // publish the pieces not yet signalled (release: orders their partial stores)
   if (lane == 0) {
-    if (split_first >= 0 && !first_sent) old_first = atom_add_acq_rel(counters + (int64_t)split_first * 8 + warp);
-    if (split_last >= 0) old_last = atom_add_acq_rel(counters + (int64_t)split_last * 8 + warp);
-  }
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int r = k == 0 ? split_first : split_last;
-    if (r < 0) continue;
-    const int lo = __ldg(prefix + r), hi = __ldg(prefix + r + 1);
-    const int c_first = (int)cta_of(lo, G, N), c_last = (int)cta_of(hi - 1, G, N);
-    int last = 0;
-    if (lane == 0) {
-      last = (k == 0 ? old_first : old_last) == c_last - c_first;
-      if (last) counters[(int64_t)r * 8 + warp] = 0;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) continue;
-    const int32_t* rec = dec + (int64_t)r * TIM_DEC_FIELDS;
-    merge_pieces<D, HKV, HG, WPH>(ws_o, ws_ml, out, r, warp, c_first, c_last, __ldg(rec + 0),
-                                  __ldg(rec + 3), __ldg(rec + 5), hq, lane);
+    if (pend0 >= 0 && !sent0) red_add_release(counters + (int64_t)pend0 * 8 + warp);
+    if (pend1 >= 0) red_add_release(counters + (int64_t)pend1 * 8 + warp);
   }
   if (trace && threadIdx.x == 0) trace[4 * blockIdx.x + 3] = gtimer();
 }

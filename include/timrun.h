@@ -186,7 +186,8 @@ int32_t tim_extend_queries_per_item(int32_t hq, int32_t hkv, int32_t head_dim, i
 int32_t tim_extend_head_groups(int32_t hq, int32_t hkv, int32_t head_dim);
 
 /* Diagnostics: per-CTA %globaltimer timeline of tim_attn_decode written to
- * buf[4*cta .. 4*cta+3] = {start, first stage landed, main loop end, end};
+ * buf[8*cta .. 8*cta+6] = {start, first stage landed, main loop end, end,
+ * producer: first tile known, first page ids in hand, first stage issued};
  * pass NULL to disable. */
 int32_t tim_set_trace(void* buf);
 /* Diagnostics: an empty grid launched like the attention kernel (n_ctas x

@@ -54,7 +54,7 @@ struct AttnCfg {
 };
 
 // Optional per-CTA timeline (%globaltimer, ns): [start, first data, loop end,
-// end] for CTA c at g_trace[4c..4c+3]; enabled by tim_set_trace (diagnostics).
+// end, producer stamps] for CTA c at g_trace[8c..8c+6]; enabled by tim_set_trace (diagnostics).
 __device__ unsigned long long* g_trace = nullptr;
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -194,7 +194,7 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
   int32_t* s_ids = reinterpret_cast<int32_t*>(empty + C::STAGES);
 
   unsigned long long* trace = g_trace;
-  if (trace && threadIdx.x == 0) trace[4 * blockIdx.x] = gtimer();
+  if (trace && threadIdx.x == 0) trace[8 * blockIdx.x] = gtimer();
   // per-step plan (tim_attn_plan): this CTA's first tile, read in the same
   // round trip as the header instead of searched for afterwards
   int4 ph = make_int4(0, 0, 0, 0), pa = ph, pb = ph;
@@ -288,24 +288,36 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
     } else {
       more = open_tile(r0);
     }
+    if (trace && lane == 0) {
+      asm volatile("" ::"r"(slot_cur), "r"(c0));   // stamp once the first tile's fields arrived
+      trace[8 * blockIdx.x + 4] = gtimer();
+    }
     if (more) fetch();
+    bool first_chunk = true;
     while (more) {
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < IPL; ++j) s_ids[lane + 32 * j] = idr[j];
+      if (trace && first_chunk && lane == 0) trace[8 * blockIdx.x + 5] = gtimer();
       __syncwarp();
       const int cur_c0 = c0, cur_c1 = c1;
       const int fresh = fresh_cur;
       const int64_t hoff = (int64_t)hgrp_cur * HG * D;   // head-group slice
-      // advance the cursor and start the next chunk's id loads
-      if (c1 < p1) {
-        c0 = c1;
-        c1 = (p1 - c0) < kIdChunk ? p1 : c0 + kIdChunk;
-        more = true;
-      } else {
-        more = open_tile(r + 1);
-      }
-      if (more) fetch();
+      // Advance the cursor and start the next chunk's id loads once this
+      // chunk's first stage is out: opening the next tile may wait on the
+      // tile batch, which must not delay the first copies of the CTA.
+      bool advanced = false;
+      auto advance = [&]() {
+        if (c1 < p1) {
+          c0 = c1;
+          c1 = (p1 - c0) < kIdChunk ? p1 : c0 + kIdChunk;
+          more = true;
+        } else {
+          more = open_tile(r + 1);
+        }
+        if (more) fetch();
+        advanced = true;
+      };
       for (int k0 = cur_c0; k0 < cur_c1; k0 += C::TK, ++it) {
         const int ntok = (cur_c1 - k0) < C::TK ? (cur_c1 - k0) : C::TK;
         const int stg = it % C::STAGES;
@@ -325,7 +337,14 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
         uint8_t* base = smem + stg * C::STAGE_BYTES + (lane >= C::TK ? C::TK * C::ROW_STRIDE : 0);
         const __nv_bfloat16* src = (lane >= C::TK ? vl : kl) + (int64_t)page * (HKV * D) + hoff;
         bulk_g2s(base + row * C::ROW_STRIDE, src, C::ROW_BYTES, &full[stg]);
+        if (trace && first_chunk && lane == 0 && k0 == cur_c0) trace[8 * blockIdx.x + 6] = gtimer();
+        if (!advanced) {
+          __syncwarp();   // the copies read s_ids: fetch() only fills registers, s_ids is rewritten next chunk
+          advance();
+        }
       }
+      if (!advanced) advance();
+      first_chunk = false;
     }
     return;
   }
@@ -418,7 +437,7 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
       const int ntok = (p1 - k0) < C::TK ? (p1 - k0) : C::TK;
       const int stg = it % C::STAGES;
       mbar_wait(&full[stg], (it / C::STAGES) & 1);
-      if (trace && it == 0 && threadIdx.x == 0) trace[4 * blockIdx.x + 1] = gtimer();
+      if (trace && it == 0 && threadIdx.x == 0) trace[8 * blockIdx.x + 1] = gtimer();
       const uint32_t kbase = smem_base + stg * C::STAGE_BYTES + hloc * D * 2;
       const uint32_t vbase = kbase + C::TK * C::ROW_STRIDE;
 
@@ -493,7 +512,7 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
       if (lane == 0) mbar_arrive(&empty[stg]);
     }
 
-    if (trace && threadIdx.x == 0) trace[4 * blockIdx.x + 2] = gtimer();
+    if (trace && threadIdx.x == 0) trace[8 * blockIdx.x + 2] = gtimer();
     // ------------------------------------------------------------ epilogue
     // Per warp, no CTA barrier.  A tile covered by one CTA is written
     // directly.  A split tile is merged (K6) by its designated piece: the one
@@ -582,7 +601,7 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
     if (pend0 >= 0 && !sent0) red_add_release(counters + (int64_t)pend0 * 8 + warp);
     if (pend1 >= 0) red_add_release(counters + (int64_t)pend1 * 8 + warp);
   }
-  if (trace && threadIdx.x == 0) trace[4 * blockIdx.x + 3] = gtimer();
+  if (trace && threadIdx.x == 0) trace[8 * blockIdx.x + 3] = gtimer();
 }
 
 template <int D, int HKV, int HG, int WPH>

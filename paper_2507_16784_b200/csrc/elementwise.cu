@@ -6,7 +6,7 @@ namespace tim {
 
 // Vector of V elements of T moved as one 16-byte access.
 template <typename T>
-struct Vec {
+struct alignas(16) Vec {
   static constexpr int V = 16 / sizeof(T);
   T v[V];
 };
@@ -47,14 +47,14 @@ TIM_DEV float block_sum(float v) {
 // out[i+half] = x1*sin + x2*cos.  Items beyond NT*MAXI per row (larger
 // models) take a second, unbuffered pass.
 template <typename T, int NT, int MAXI>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, 3)
     rope_kv_kernel(const T* __restrict__ qkv, const T* __restrict__ h, int dm, float eps,
                    const int32_t* __restrict__ row_pos, const int32_t* __restrict__ row_pages,
                    const float* __restrict__ cos_tab, const float* __restrict__ sin_tab, int hq,
                    int hkv, int D, T* __restrict__ q_out, T* __restrict__ k_layer,
                    T* __restrict__ v_layer) {
   constexpr int V = Vec<T>::V;
-  constexpr int MAXH = 4;
+  constexpr int MAXH = 16 / V;   // dm <= 4096 in registers; wider rows take the loop below
   griddep_launch();   // the attention kernel may start streaming old pages now
   griddep_wait();     // qkv / h come from the preceding GEMM (programmatic launch)
   const int r = blockIdx.x;
@@ -167,10 +167,10 @@ __global__ void __launch_bounds__(NT)
 // the W1 GEMM (model.py:161).  One CTA per row, all loads issued before the
 // reduction (one round trip); widths beyond NT*V*MAXU take a second pass.
 template <typename T, int NT, int MAXU>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, 3)
     silu_rms_kernel(T* __restrict__ u, int width, const T* __restrict__ h, int dm, float eps) {
   constexpr int V = Vec<T>::V;
-  constexpr int MAXH = 4;
+  constexpr int MAXH = 16 / V;   // dm <= 4096 in registers; wider rows take the loop below
   griddep_launch();   // the down-projection GEMM may start streaming its weights
   griddep_wait();     // u / h come from the preceding GEMM (programmatic launch)
   const int r = blockIdx.x;

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--dump", action="store_true")
+    ap.add_argument("--no-plan", action="store_true", help="skip tim_attn_plan (K1 searches itself)")
     ap.add_argument("--isolated", action="store_true",
                     help="CUDA events around every launch (as bench.py times layer 0): no PDL overlap")
     a = ap.parse_args()
@@ -48,6 +49,7 @@ def main():
     sd = StepDesc()
     for i, n in enumerate(lens):
         sd.dec.append((i, i, int(n), 1, int(n) - 1, 0))
+    sd.serial = 0 if a.no_plan else 1
     step = torch.from_numpy(sd.pack()).cuda()
     q = torch.randn(a.batch, hq, d, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)
@@ -55,6 +57,8 @@ def main():
     ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, a.batch, hkv, d), device="cuda")
     cnt = torch.zeros(a.batch * 8, dtype=torch.int32, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
+    if not a.no_plan:   # the per-step plan the engine computes once per step
+        L.call("tim_attn_plan", step.data_ptr(), ctas, a.batch, d, ws.data_ptr(), st)
 
     def run(l):
         L.call("tim_attn_decode", step.data_ptr(), 0, q.data_ptr(), out.data_ptr(), K[l].data_ptr(),
@@ -86,16 +90,17 @@ def main():
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) / a.layers)
     if a.trace:
-        tr = torch.zeros(ctas * 4, dtype=torch.int64, device="cuda")
+        tr = torch.zeros(ctas * 8, dtype=torch.int64, device="cuda")
         L.call("tim_set_trace", tr.data_ptr())
         run(0)
         torch.cuda.synchronize()
         L.call("tim_set_trace", None)
-        t = tr.view(-1, 4).cpu().numpy().astype(np.float64)
+        t = tr.view(-1, 8).cpu().numpy().astype(np.float64)[:, :7]
         t0 = t[:, 0].min()
         t = (t - t0) / 1000.0
         print(json.dumps({k: [round(float(np.percentile(t[:, i], p)), 2) for p in (0, 50, 100)]
-                          for i, k in enumerate(["start", "first", "loop_end", "end"])}))
+                          for i, k in enumerate(["start", "first", "loop_end", "end", "p_tile", "p_ids",
+                                                 "p_issue"])}))
         if a.dump:
             pre = np.concatenate([[0], np.cumsum(lens)])
             N = int(pre[-1])

@@ -179,6 +179,14 @@ def run_gpu(args, rank: int, world: int, dist):
     records, rt.recording = rt.recording, None
     resident = rt.replay_upload(records)
     rows = sorted(sd.n_rows for sd, _, _ in records)
+    if os.environ.get("TIMRUN_STEPSTATS"):
+        for sd, _, _ in records:
+            if sd.ext:
+                segs = [sg[2] for sg in sd.segs if sg[2] > 1]
+                print(f"[step] rows={sd.n_rows} dec_tiles={len(sd.dec)} dec_keys={sum(d[2] for d in sd.dec)} "
+                      f"ext_items={len(sd.ext)} ext_blocks={sum((e[2] + 63) // 64 for e in sd.ext)} "
+                      f"split={sd.offsets.get('split_dec_ctas')}/{sd.offsets.get('split_ext_ctas')} "
+                      f"multi_segs={sorted(segs)[:12]}", file=sys.stderr)
     launches0 = rt.launches
     rt.attn_events, rt.phase_events = attn_store, phase_store
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
@@ -284,6 +292,10 @@ def run_gpu(args, rank: int, world: int, dist):
     attn_bytes = sum(sum(sg[1] + sg[2] for sg in sd.segs) * kv_tok_layer + sd.n_rows * q_o_bytes
                      for _, sd in attn) / max(len(attn), 1)
     dec_only = [(t, sd) for t, sd in attn if sd.n_rows == len(sd.segs)]
+    mixed = [(t, sd) for t, sd in attn if sd.n_rows != len(sd.segs)]
+    mix_ms = sum(t for t, _ in mixed) / max(len(mixed), 1)
+    mix_bytes = sum(sum(sg[1] + sg[2] for sg in sd.segs) * kv_tok_layer + sd.n_rows * q_o_bytes
+                    for _, sd in mixed) / max(len(mixed), 1)
     dec_ms = sum(t for t, _ in dec_only) / max(len(dec_only), 1)
     dec_bytes = sum(sum(sg[1] + sg[2] for sg in sd.segs) * kv_tok_layer + sd.n_rows * q_o_bytes
                     for _, sd in dec_only) / max(len(dec_only), 1)
@@ -297,6 +309,7 @@ def run_gpu(args, rank: int, world: int, dist):
     return dict(ms=ms, e2e_ms=e2e_ms, wall_ms=wall_ms, tokens=planned_tokens, e2e_tokens=e2e_tokens,
                 attn_ms=attn_ms, attn_bytes=attn_bytes, launches=launches, clocks=clk,
                 dec_ms=dec_ms, dec_bytes=dec_bytes, n_dec_launches=len(dec_only), n_attn=len(attn),
+                mix_ms=mix_ms, mix_bytes=mix_bytes, n_mix_launches=len(mixed),
                 h2d=h2d / args.steps, d2h=d2h / args.steps, mean_live=mean_live,
                 weight_gb=weight_gb, floor_ms=floor_ms)
 
@@ -477,7 +490,12 @@ def main():
                                                if res["dec_ms"] else None,
                                                "bytes_per_launch": res["dec_bytes"],
                                                "ms_per_launch": res["dec_ms"],
-                                               "launches": res["n_dec_launches"]}},
+                                               "launches": res["n_dec_launches"]},
+                         "mixed_steps": {"achieved": (res["mix_bytes"] / (res["mix_ms"] * 1e-3) / 1e9)
+                                         if res["mix_ms"] else None,
+                                         "bytes_per_launch": res["mix_bytes"],
+                                         "ms_per_launch": res["mix_ms"],
+                                         "launches": res["n_mix_launches"]}},
             "cpu_baseline": cpu,
             "e2e": {"value": res["e2e_tokens"] / (res["e2e_ms"] * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],

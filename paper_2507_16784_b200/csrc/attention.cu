@@ -234,6 +234,7 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
   TileLane tl;
   tl.load(prefix, dec, n_dec, r0, lane);
   __syncthreads();
+  if (warp > NW) return;   // spare warps of a wider (one-launch) CTA
 
   if (warp == NW) {
     // ------------------------------------------------------------ producer
@@ -632,7 +633,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 // dependent launch after the RoPE/store kernel, which two launches on forked
 // streams would lose.
 template <int D, int HKV>
-__global__ void __launch_bounds__(AttnCfg<D, HKV, 1>::THREADS, 1)
+constexpr int step_threads() {
+  return AttnCfg<D, HKV, 1>::THREADS > tc::THREADS ? AttnCfg<D, HKV, 1>::THREADS : tc::THREADS;
+}
+
+template <int D, int HKV>
+__global__ void __launch_bounds__(step_threads<D, HKV>(), 1)
     attn_step_kernel(const int32_t* __restrict__ step, const __nv_bfloat16* __restrict__ q,
                      __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kl,
                      const __nv_bfloat16* __restrict__ vl, const int32_t* __restrict__ tables,
@@ -804,7 +810,7 @@ int32_t launch_step(const int32_t* step, const void* q, void* out, const void* k
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_ctas);
-  cfg.blockDim = dim3(AttnCfg<D, HKV, 1>::THREADS);
+  cfg.blockDim = dim3(step_threads<D, HKV>());
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = st;
   cfg.attrs = attrs;
@@ -848,7 +854,7 @@ extern "C" int32_t tim_attn_plan(const int32_t* step, int32_t n_ctas, int32_t ma
 
 extern "C" int32_t tim_extend_queries_per_item(int32_t hq, int32_t hkv, int32_t head_dim, int32_t dtype) {
   // queries per multi-token attention tile (mode 1 of tim_attn_decode)
-  if (dtype == TIM_DTYPE_BF16 && ext_tc_shape(hq, hkv, head_dim)) return 128 / (hq / hkv);
+  if (dtype == TIM_DTYPE_BF16 && ext_tc_shape(hq, hkv, head_dim)) return tc::QBLK * tc::M / (hq / hkv);
   if (dtype == TIM_DTYPE_BF16 && tensor_core_shape(hq, hkv, head_dim))
     return (8 / ext_hg(hkv)) * (16 / (hq / hkv));
   return 1 << 30;  // generic path: whole segments

@@ -9,21 +9,23 @@
 // whole page rows for 4 queries per tile, so a 150-row re-encode re-reads its
 // ~700-token prefix ~38 times, and its per-warp m16n8k16 chains are latency
 // bound (ncu: HMMA pipe <20 % busy, consumers starved on a 3-stage ring).  Here
-// one work item is (query block of 32 queries x the 4 q heads of one kv head)
-// = 128 MMA rows, so each kv head's K/V slice is streamed once per 32 queries,
-// and S = Q K^T / O += P V are single-thread tcgen05.mma issues
-// (M=128, N=64 / N=128) with fp32 accumulators in TMEM.
+// one work item is 64 queries x the 4 q heads of one kv head = two q-blocks of
+// 128 MMA rows that share every K/V block, so each kv head's K/V slice is
+// streamed once per 64 queries, and S = Q K^T / O += P V are single-thread
+// tcgen05.mma issues (M=128, N=64 / N=128 per q-block) with fp32 accumulators
+// in TMEM (all 512 columns).
 //
 // Per CTA (persistent, one per SM, items round-robin):
-//   warp 5     producer: page ids -> 16-byte cp.async of the kv head's 256-byte
-//              K and V rows into a 4-stage ring of 64-token blocks, stored
+//   warp 9     producer: page ids -> 16-byte cp.async of the kv head's 256-byte
+//              K and V rows into a 3-stage ring of 64-token blocks, stored
 //              128B-swizzled, i.e. the canonical UMMA layouts (K: K-major B
 //              operand, V: MN-major B).  (TMA tile::gather4 does the same with
 //              128-byte rows but was measured ~10x slower per byte here.)
-//   warp 4     MMA issuer (one thread): S_j = Q K_j^T into one of two TMEM S
-//              buffers, O += P_j V_j into the TMEM O accumulator.
-//   warps 0-3  softmax / epilogue, thread t <-> TMEM lane t <-> MMA row t
-//              (query t/4, head t%4 of the kv head): tcgen05.ld of its 64
+//   warp 8     MMA issuer (one thread): S_j = Q K_j^T into one of two TMEM S
+//              buffers per q-block, O += P_j V_j into the q-block's O.
+//   warps 0-7  softmax / epilogue, warps 4b..4b+3 own q-block b; thread t <->
+//              TMEM lane t <-> MMA row t of its q-block (query t/4, head t%4 of
+//              the kv head): tcgen05.ld of its 64
 //              scores, causal mask, online softmax in the log2 domain with
 //              lazy rescaling (O is rescaled in TMEM only when the running max
 //              grows by more than 2^8), P as bf16 into a swizzled smem tile
@@ -37,7 +39,8 @@ constexpr int D = 128;               // head dim (two 64-element, 128-byte slabs
 constexpr int GRP = 4;               // q heads per kv head
 constexpr int M = 128;               // MMA rows per item
 constexpr int BN = 64;               // keys per block
-constexpr int ST = 4;                // K/V ring stages
+constexpr int QBLK = 2;              // q-blocks per item: two MMA row tiles share each K/V block
+constexpr int ST = 3;                // K/V ring stages
 constexpr int Q_SLAB = M * 128;      // 16 KiB
 constexpr int Q_BYTES = 2 * Q_SLAB;  // 32 KiB
 constexpr int P_BYTES = M * 128;     // 16 KiB (128 rows x 64 keys bf16)
@@ -45,10 +48,11 @@ constexpr int KV_SLAB = BN * 128;    // 8 KiB (64 keys x 64 elements)
 constexpr int K_BYTES = 2 * KV_SLAB;
 constexpr int STAGE = 2 * K_BYTES;   // K then V, 32 KiB
 constexpr int BAR_BYTES = 256;
-constexpr int SMEM = 1024 + 2 * Q_BYTES + 2 * P_BYTES + ST * STAGE + BAR_BYTES;
-constexpr int THREADS = 6 * 32;
-constexpr int TMEM_COLS = 256;       // S[2] (64 cols each) + O (128 cols)
-constexpr uint32_t O_COL = 128;
+constexpr int SMEM = 1024 + QBLK * Q_BYTES + 2 * QBLK * P_BYTES + ST * STAGE + BAR_BYTES;
+constexpr int THREADS = 10 * 32;     // 8 softmax warps (4 per q-block), MMA, producer
+constexpr int MMA_WARP = 8, PROD_WARP = 9;
+constexpr int TMEM_COLS = 512;       // S[2 buffers][2 q-blocks] (64 cols each) + O[2 q-blocks] (128 cols)
+constexpr uint32_t O_COL = 256;
 constexpr float kRescaleLog2 = 8.f;  // lazy rescale threshold (p <= 2^8 with a stale max)
 
 // kind::f16 instruction descriptors (bf16 x bf16 -> f32, M = 128)
@@ -127,16 +131,16 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
                          int64_t tstride, int hq, int hkv, float scale_log2, int cta, int grid) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sP = sQ + 2 * Q_BYTES;           // Q is double-buffered (next item prefetched)
-  uint8_t* sKV = sP + 2 * P_BYTES;
+  uint8_t* sQ = smem;                       // [q-block] 32 KiB A tiles
+  uint8_t* sP = sQ + QBLK * Q_BYTES;        // [buffer][q-block] 16 KiB P tiles
+  uint8_t* sKV = sP + 2 * QBLK * P_BYTES;
   uint64_t* kv_full = reinterpret_cast<uint64_t*>(sKV + ST * STAGE);
   uint64_t* kv_empty = kv_full + ST;
   uint64_t* s_ready = kv_empty + ST;   // [2]
   uint64_t* p_ready = s_ready + 2;     // [2]
   uint64_t* pv_done = p_ready + 2;     // [2]
-  uint64_t* q_ready = pv_done + 2;     // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_ready + 2);
+  uint64_t* q_ready = pv_done + 2;     // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_ready + 1);
 
   unsigned long long* tr = cta == 0 ? g_tc_trace : nullptr;
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
@@ -155,14 +159,13 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_ready[b], 1);
-      mbar_init(&p_ready[b], M);
+      mbar_init(&p_ready[b], QBLK * M);
       mbar_init(&pv_done[b], 1);
     }
-    mbar_init(&q_ready[0], M);
-    mbar_init(&q_ready[1], M);
+    mbar_init(q_ready, QBLK * M);
     fence_mbar_init();
   }
-  if (warp == 4) {
+  if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)), "n"(TMEM_COLS)
                  : "memory");
@@ -173,7 +176,7 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 5) {
+  if (warp == PROD_WARP) {
     // ---------------------------------------------------------- producer
     // 16-byte cp.async (LDGSTS) of the kv head's 256-byte K and V rows into
     // the swizzled slabs: a warp instruction moves two whole rows, where a TMA
@@ -221,7 +224,7 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
       }
     }
     cp_async_wait<0>();
-  } else if (warp == 4) {
+  } else if (warp == MMA_WARP) {
     // ---------------------------------------------------------- MMA issuer
     // Event loop over two cursors: the next S_g = Q K_g^T (needs its K block
     // and its item's Q, and S buffer g&1 released, i.e. PV_{g-2} issued) and
@@ -232,25 +235,33 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
       auto nblk_of = [&](int it) {
         return it < n_items ? (items[(int64_t)it * TIM_EXT_FIELDS + 2] + BN - 1) / BN : 0;
       };
-      int s_it = cta, s_j = 0, s_g = 0, s_ii = 0, s_nb = nblk_of(s_it);
-      int p_it = cta, p_j = 0, p_g = 0, p_nb = s_nb;
+      auto nqb_of = [&](int it) {   // q-blocks holding queries (an item of <= 32 queries has one)
+        return it < n_items ? (items[(int64_t)it * TIM_EXT_FIELDS + 3] + M / GRP - 1) / (M / GRP) : 0;
+      };
+      int s_it = cta, s_j = 0, s_g = 0, s_ii = 0, s_nb = nblk_of(s_it), s_nqb = nqb_of(s_it);
+      int p_it = cta, p_j = 0, p_g = 0, p_nb = s_nb, p_nqb = s_nqb;
       bool q_ok = false;
       while (p_it < n_items) {
         bool progress = false;
         if (s_it < n_items && s_g <= p_g + 1) {
-          if (!q_ok && mbar_test(&q_ready[s_ii & 1], (s_ii >> 1) & 1)) q_ok = true;
+          if (!q_ok && mbar_test(q_ready, s_ii & 1)) q_ok = true;
           const int stg = s_g % ST;
           if (q_ok && mbar_test(&kv_full[stg], (s_g / ST) & 1)) {
             TCT(2, s_g);
             fence_proxy_async();          // cp.async (generic proxy) data -> tensor-core reads
             fence_after();
-            const uint32_t qb = qa + (s_ii & 1) * Q_BYTES, kb = kva + stg * STAGE;
-            const uint32_t d = tmem + (uint32_t)((s_g & 1) * BN);
+            const uint32_t kb = kva + stg * STAGE;
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint32_t off = (kk & 3) * 32;
-              mma_ss(d, desc_sw128(qb + (kk >> 2) * Q_SLAB + off, 16, 1024),
-                     desc_sw128(kb + (kk >> 2) * KV_SLAB + off, 16, 1024), kIdescS, kk > 0);
+            for (int qblk = 0; qblk < QBLK; ++qblk) {
+              if (qblk >= s_nqb) break;
+              const uint32_t qb = qa + qblk * Q_BYTES;
+              const uint32_t d = tmem + (uint32_t)(((s_g & 1) * QBLK + qblk) * BN);
+#pragma unroll
+              for (int kk = 0; kk < D / 16; ++kk) {
+                const uint32_t off = (kk & 3) * 32;
+                mma_ss(d, desc_sw128(qb + (kk >> 2) * Q_SLAB + off, 16, 1024),
+                       desc_sw128(kb + (kk >> 2) * KV_SLAB + off, 16, 1024), kIdescS, kk > 0);
+              }
             }
             commit(&s_ready[s_g & 1]);
             ++s_g;
@@ -260,6 +271,7 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
               ++s_ii;
               q_ok = false;
               s_nb = nblk_of(s_it);
+              s_nqb = nqb_of(s_it);
             }
             progress = true;
           }
@@ -270,9 +282,12 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
           fence_after();
           const uint32_t vb = kva + (p_g % ST) * STAGE + K_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk)
-            mma_ss(tmem + O_COL, desc_sw128(pa + b * P_BYTES + kk * 32, 16, 1024),
-                   desc_sw128(vb + kk * 2048, KV_SLAB, 1024), kIdescO, (p_j > 0 || kk > 0) ? 1u : 0u);
+          for (int qblk = 0; qblk < QBLK; ++qblk)
+#pragma unroll
+            for (int kk = 0; kk < BN / 16; ++kk)
+              if (qblk < p_nqb)
+              mma_ss(tmem + O_COL + qblk * D, desc_sw128(pa + (b * QBLK + qblk) * P_BYTES + kk * 32, 16, 1024),
+                     desc_sw128(vb + kk * 2048, KV_SLAB, 1024), kIdescO, (p_j > 0 || kk > 0) ? 1u : 0u);
           commit(&pv_done[b]);
           commit(&kv_empty[p_g % ST]);
           ++p_g;
@@ -280,25 +295,28 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
             p_j = 0;
             p_it += grid;
             p_nb = nblk_of(p_it);
+            p_nqb = nqb_of(p_it);
           }
           progress = true;
         }
         if (!progress) __nanosleep(20);
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < 4 * QBLK) {
     // ---------------------------------------------------------- softmax
-    const int t = threadIdx.x;                       // MMA row / TMEM lane
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-    const int qi = t / GRP, hj = t % GRP;
+    const int qblk = warp >> 2;                      // this warp's q-block
+    const int t = threadIdx.x & (M - 1);             // MMA row / TMEM lane within the q-block
+    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t s_col = (uint32_t)(qblk * BN), o_col = O_COL + (uint32_t)(qblk * D);
+    const int qi = qblk * (M / GRP) + t / GRP, hj = t % GRP;
     griddep_wait();                                  // q rows come from the preceding kernel
-    // Q row t of item `it` -> swizzled K-major A tile in buffer qb (cp.async,
-    // completion counted on q_ready[qb]); issued one item ahead.
-    auto load_q = [&](int it, int qb) {
+    // Q row t of this q-block of item `it` -> swizzled K-major A tile (cp.async,
+    // completion counted on q_ready); the previous item's MMAs are all done.
+    auto load_q = [&](int it) {
       const int32_t* rec = items + (int64_t)it * TIM_EXT_FIELDS;
       const bool ok = qi < rec[3];
       const __nv_bfloat16* src = q + ((int64_t)(rec[0] + (ok ? qi : 0)) * hq + rec[5] * GRP + hj) * D;
-      uint8_t* dq = sQ + qb * Q_BYTES;
+      uint8_t* dq = sQ + qblk * Q_BYTES;
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         uint8_t* dst = dq + (c >> 3) * Q_SLAB + swz(t, c & 7);
@@ -306,10 +324,8 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
         else *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
       }
       if (!ok) fence_proxy_async();
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&q_ready[qb]))
-                   : "memory");
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(q_ready)) : "memory");
     };
-    load_q(cta, 0);
     int gb = 0, ii = 0;
     for (int it = cta; it < n_items; it += grid, ++ii) {
       const int32_t* rec = items + (int64_t)it * TIM_EXT_FIELDS;
@@ -318,20 +334,30 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
       const bool valid = qi < nq;
       const int lim = kv_len - nq + qi;              // last key this query sees (model.py:139-140)
       const int64_t qoff = ((int64_t)(row0 + qi) * hq + head * GRP + hj) * D;
-      // the other Q buffer's last reader (item ii-1) has completed: prefetch
-      if (it + (int)grid < n_items) load_q(it + grid, (ii + 1) & 1);
+      load_q(it);
 
+      if (qblk * (M / GRP) >= nq) {
+        // this q-block holds no query of the item: no MMA was issued for it,
+        // its warps only keep the barrier phases (arrive once S_j exists, so
+        // the arrival cannot count toward block j-2's phase)
+        for (int j = 0; j < nblk; ++j, ++gb) {
+          mbar_wait(&s_ready[gb & 1], (gb >> 1) & 1);
+          mbar_arrive(&p_ready[gb & 1]);
+        }
+        mbar_wait(&pv_done[(gb - 1) & 1], ((gb - 1) >> 1) & 1);   // item done before the next Q
+        continue;
+      }
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < nblk; ++j, ++gb) {
         const int b = gb & 1;
         mbar_wait(&s_ready[b], (gb >> 1) & 1);
-        if (t == 0) TCT(4, gb);
+        if (threadIdx.x == 0) TCT(4, gb);
         fence_after();
         float s[64];
         {
           float a0[32], a1[32];
-          tld32(lane_base + (uint32_t)(b * BN), a0);
-          tld32(lane_base + (uint32_t)(b * BN + 32), a1);
+          tld32(lane_base + (uint32_t)(b * QBLK * BN) + s_col, a0);
+          tld32(lane_base + (uint32_t)(b * QBLK * BN) + s_col + 32, a1);
           tld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -381,22 +407,22 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
 #pragma unroll
           for (int cblk = 0; cblk < D / 32; ++cblk) {
             float o[32];
-            tld32(lane_base + O_COL + cblk * 32, o);
+            tld32(lane_base + o_col + cblk * 32, o);
             tld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] *= corr;
-            tst32(lane_base + O_COL + cblk * 32, o);
+            tst32(lane_base + o_col + cblk * 32, o);
           }
           tst_wait();
         }
-        uint8_t* prow = sP + b * P_BYTES;
+        uint8_t* prow = sP + (b * QBLK + qblk) * P_BYTES;
 #pragma unroll
         for (int c = 0; c < 8; ++c)
           *reinterpret_cast<uint4*>(prow + swz(t, c)) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         fence_proxy_async();
         fence_before();
         mbar_arrive(&p_ready[b]);
-        if (t == 0) TCT(5, gb);
+        if (threadIdx.x == 0) TCT(5, gb);
       }
       // epilogue: O / l of this row -> bf16 -> out
       const int gl = gb - 1;
@@ -407,7 +433,7 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
 #pragma unroll
       for (int cblk = 0; cblk < D / 32; ++cblk) {
         float o[32];
-        tld32(lane_base + O_COL + cblk * 32, o);
+        tld32(lane_base + o_col + cblk * 32, o);
         tld_wait();
         if (valid) {
 #pragma unroll
@@ -426,7 +452,7 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
   }
   fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == MMA_WARP) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS)
                  : "memory");

@@ -390,9 +390,10 @@ class B200Transformer:
             hq, hkv, D, L.DTYPE_BF16) < (1 << 30))
         self.tile_q = 16 // (hq // hkv) if self.tensor_cores else 0   # queries per mode-0 tile
         # multi-token rows go to the tcgen05 kernel (mode 1) when the shape has
-        # one: 128 MMA rows = ext_q queries x the q heads of one kv head
+        # one: an item = ext_q queries x the q heads of one kv head (two 128-row
+        # MMA tiles sharing each K/V block)
         qpi = L.load().tim_extend_queries_per_item(hq, hkv, D, L.DTYPE_BF16) if self.tensor_cores else 0
-        self.ext_q = qpi if self.tensor_cores and qpi * (hq // hkv) == 128 else 0
+        self.ext_q = qpi if self.tensor_cores and qpi * (hq // hkv) in (128, 256) else 0
         self.ext_groups = L.load().tim_extend_head_groups(hq, hkv, D) if self.ext_q else 0
         self._runtimes: dict[int, StepRuntime] = {}
 

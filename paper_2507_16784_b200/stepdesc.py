@@ -6,6 +6,8 @@ buffer every kernel of the step reads (include/timrun.h).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib as L
@@ -58,12 +60,15 @@ class StepDesc:
             self.spans.extend((a, b))
         self.jobs.append((slot, old_len, s, reencode_from, off, len(spans), out_row, keep))
 
-    # Cost model of the one-launch attention (mode 2), in SM-microseconds
-    # measured on B200: a decode-tile CTA streams ~44 KB/us of page rows; a
-    # multi-token item costs ~2 us plus ~0.95 us per 64-key block.
-    DEC_US_PER_TOKEN = 4096 / 44e3
-    EXT_US_PER_BLOCK = 0.95
-    EXT_US_PER_ITEM = 2.0
+    # Cost model of the one-launch attention (mode 2), in SM-microseconds,
+    # calibrated on B200 with tools/attn_mixed_bench.py (mode 2, decode CTAs
+    # streaming next to the items): a decode-tile CTA streams ~40 KB/us of
+    # page rows; a multi-token item costs ~4 us (Q load, epilogue) plus ~1.6 us
+    # per 64-key block for each of its (up to two) 32-query blocks; items are
+    # dealt longest-first, round-robin.  TIMRUN_EXT_COST="item,block" overrides.
+    DEC_US_PER_TOKEN = 4096 / 40e3
+    EXT_US_PER_ITEM, EXT_US_PER_QBLOCK_BLOCK = (
+        float(x) for x in os.environ.get("TIMRUN_EXT_COST", "4.0,1.6").split(","))
 
     def attention_split(self) -> tuple[int, int]:
         """CTAs given to the decode tiles and to the multi-token items when
@@ -74,8 +79,8 @@ class StepDesc:
         if not self.dec:
             return (0, G)
         w0 = sum(d[2] for d in self.dec) * self.DEC_US_PER_TOKEN
-        times = sorted((self.EXT_US_PER_ITEM + self.EXT_US_PER_BLOCK * ((e[2] + 63) // 64)
-                        for e in self.ext), reverse=True)
+        times = sorted((self.EXT_US_PER_ITEM + self.EXT_US_PER_QBLOCK_BLOCK * ((e[3] + 31) // 32)
+                        * ((e[2] + 63) // 64) for e in self.ext), reverse=True)
         n = len(times)
         best, best_g1 = None, 1
         for g1 in range(1, min(G - 1, n) + 1):

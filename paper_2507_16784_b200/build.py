@@ -36,7 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     cmd = [
         nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-        "--expt-relaxed-constexpr", "-I", str(ROOT / "include"), "-I", str(CSRC),
+        "--expt-relaxed-constexpr", *os.environ.get("TIMRUN_NVCC_FLAGS", "").split(), "-I", str(ROOT / "include"), "-I", str(CSRC),
         "-o", str(LIB) + ".tmp", *[str(CSRC / s) for s in SOURCES], "-lcudart",
     ]
     if verbose:

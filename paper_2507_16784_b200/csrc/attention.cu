@@ -331,6 +331,10 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
           griddep_wait();
           waited = true;
         }
+#ifdef TIM_CONSUMER_ONLY
+        if (lane == 0) mbar_arrive(&full[stg]);   // diagnostics: no copies (tools/consumer_only_probe.sh)
+        continue;
+#endif
         if (lane == 0) mbar_arrive_expect_tx(&full[stg], 2 * C::TK * C::ROW_BYTES);
         __syncwarp();
         const int row = lane & (C::TK - 1);

@@ -12,7 +12,7 @@ P="ncu --profile-from-start off --clock-control none"
 M="--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv"
 timeout 900 $P $M --log-file gpurun_out/launches_decode_step.csv python tools/profile_step.py --rows 64
 timeout 900 $P $M --log-file gpurun_out/launches_mixed_step.csv python tools/profile_step.py --min-rows 600
-timeout 900 $P --set full --import-source on -k regex:attn_ -c 1 -o gpurun_out/ncu_attn_decode_step python tools/profile_step.py --rows 64
-timeout 900 $P --set full --import-source on -k regex:attn_ -c 1 -o gpurun_out/ncu_attn_mixed_step python tools/profile_step.py --min-rows 600
+timeout 900 $P --set full --import-source on -k regex:"attn_(tiles|step)" -c 1 -o gpurun_out/ncu_attn_decode_step python tools/profile_step.py --rows 64
+timeout 900 $P --set full --import-source on -k regex:"attn_(tiles|step)" -c 1 -o gpurun_out/ncu_attn_mixed_step python tools/profile_step.py --min-rows 600
 timeout 600 python tools/bench_configs.py --config c5 --skip 1500 --steps 100 > gpurun_out/c5.json
 timeout 1500 python tools/bench_configs.py --config c4 --skip 600 --steps 100 > gpurun_out/c4.json

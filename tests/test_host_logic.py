@@ -129,3 +129,70 @@ def test_step_descriptor_layout():
     assert job == [0, 5, 2, 4, 0, 1, 0, 1]
     assert arr[hdr["off_spans"]:hdr["off_spans"] + 2].tolist() == [4, 6]
     assert arr.dtype == np.int32
+
+
+def test_header_fields_match_c_struct():
+    """stepdesc._HDR is tim_step_header's field order (include/timrun.h)."""
+    import re
+    from pathlib import Path
+    text = (Path(__file__).resolve().parents[1] / "include" / "timrun.h").read_text()
+    body = re.search(r"typedef struct \{(.*?)\} tim_step_header;", text, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        for part in decl.replace("int32_t", "").split(","):
+            part = part.strip()
+            if part:
+                names.append(part)
+    fields = [n for n in names if not n.startswith("reserved")]
+    assert fields == list(_HDR)
+    reserved = int(re.search(r"reserved\[(\d+)\]", body).group(1))
+    assert len(fields) + reserved == L.HEADER_INTS
+
+
+def _ext_items(n_rows, m, heads=8, qpi=64):
+    items = []
+    for q0 in range(0, n_rows, qpi):
+        nq = min(qpi, n_rows - q0)
+        for h in range(heads):
+            items.append((q0, 0, m + q0 + nq, nq, m, h))
+    return items
+
+
+def test_attention_split_cost_model():
+    """mode-2 CTA split: degenerate lists take every CTA; otherwise both sides
+    get >= 1 CTA, the ext side never more CTAs than items, and more
+    multi-token work never gets fewer CTAs."""
+    def split(n_dec_keys, ext):
+        sd = StepDesc()
+        sd.ctas = 148
+        if n_dec_keys:
+            per = n_dec_keys // 64
+            sd.dec += [(i, i, per, 1, per - 1, 0) for i in range(64)]
+        sd.ext += ext
+        return sd.attention_split()
+
+    assert split(44000, []) == (148, 0)
+    assert split(0, _ext_items(150, 600)) == (0, 148)
+    prev = 0
+    for n_rows in (8, 40, 150, 440, 900, 1600):
+        ext = _ext_items(n_rows, 700)
+        g0, g1 = split(44000, ext)
+        assert g0 + g1 == 148 and g0 >= 1 and 1 <= g1 <= len(ext)
+        assert g1 >= prev
+        prev = g1
+
+
+def test_pack_sorts_items_and_stamps_serial():
+    sd = StepDesc()
+    sd.ext += [(0, 0, 100, 8, 92, 0), (0, 0, 700, 64, 636, 1), (0, 0, 300, 8, 292, 2)]
+    sd.serial, sd.ctas = 17, 148
+    arr = sd.pack()
+    hdr = {k: int(arr[i]) for i, k in enumerate(_HDR)}
+    assert hdr["serial"] == 17 and hdr["n_ext"] == 3
+    ext = arr[hdr["off_ext"]:hdr["off_ext"] + 3 * L.EXT_FIELDS].reshape(3, L.EXT_FIELDS)
+    assert ext[:, 2].tolist() == [700, 300, 100]       # longest first (round-robin dealing)
+    assert hdr["split_dec_ctas"] == 0 and hdr["split_ext_ctas"] == 148

@@ -175,12 +175,13 @@ int32_t tim_attn_decode(const int32_t* step, int32_t mode, const void* q, void* 
                         int64_t table_stride, int32_t hq, int32_t hkv, int32_t head_dim,
                         float scale, float* ws, int32_t* counters, int32_t n_ctas, int32_t max_dec,
                         int32_t dtype, void* stream);
-/* Per-step plan of the decode-tile partition (each K1 CTA's first tile),
- * written into the tail of `ws` once per step (the partition is the same for
- * every layer); K1 uses it when the descriptor's serial matches, else it
- * searches itself.  n_ctas / max_dec / head_dim as passed to tim_attn_decode. */
-int32_t tim_attn_plan(const int32_t* step, int32_t n_ctas, int32_t max_dec, int32_t head_dim, float* ws,
-                      void* stream);
+/* Per-step plan of the decode-tile partition (each K1 CTA's first tile and
+ * the page ids of its first two stages), written into the tail of `ws` once
+ * per step after the page ops (the partition is the same for every layer);
+ * K1 uses it when the descriptor's serial matches, else it searches itself.
+ * n_ctas / max_dec / head_dim as passed to tim_attn_decode. */
+int32_t tim_attn_plan(const int32_t* step, const int32_t* block_tables, int64_t table_stride, int32_t n_ctas,
+                      int32_t max_dec, int32_t head_dim, float* ws, void* stream);
 /* Queries per multi-token tile and kv-head groups per query for a config. */
 int32_t tim_extend_queries_per_item(int32_t hq, int32_t hkv, int32_t head_dim, int32_t dtype);
 int32_t tim_extend_head_groups(int32_t hq, int32_t hkv, int32_t head_dim);

@@ -131,7 +131,9 @@ TIM_DEV int ld_acquire(const int32_t* p) {
 // plus a tile-batch load before its first page ids; the record is used only
 // when its serial, G and N match the launch (else K1 searches as before).
 constexpr int kPlanMaxCtas = 256;
-constexpr int kPlanInts = 8 + 8 * kPlanMaxCtas;
+constexpr int kPlanIds = 32;                      // page ids of the CTA's first two stages
+constexpr int kPlanRec = 8 + kPlanIds;            // ints per CTA record
+constexpr int kPlanInts = 8 + kPlanRec * kPlanMaxCtas;
 
 TIM_DEV int64_t ws_core_floats(int n_ctas, int max_dec, int d) { return (int64_t)(n_ctas + max_dec) * 8 * 16 * (d + 2); }
 
@@ -147,8 +149,8 @@ TIM_DEV int dec_grid(const tim_step_header& hd, int n_ctas) {
   return g0;
 }
 
-__global__ void attn_plan_kernel(const int32_t* __restrict__ step, int n_ctas, int max_dec, int d,
-                                 float* __restrict__ ws) {
+__global__ void attn_plan_kernel(const int32_t* __restrict__ step, const int32_t* __restrict__ tables,
+                                 int64_t tstride, int n_ctas, int max_dec, int d, float* __restrict__ ws) {
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
   int32_t* plan = reinterpret_cast<int32_t*>(ws + ws_core_floats(n_ctas, max_dec, d));
   const int n_dec = hd.n_dec, N = hd.dec_total;
@@ -172,9 +174,14 @@ __global__ void attn_plan_kernel(const int32_t* __restrict__ step, int n_ctas, i
       if (prefix[mid] <= start) lo = mid; else hi = mid - 1;
     }
     const int32_t* rec = dec + (int64_t)lo * TIM_DEC_FIELDS;
-    int32_t* o = plan + 8 + 8 * c;
+    int32_t* o = plan + 8 + kPlanRec * c;
+    const int lo0 = prefix[lo], hi0 = prefix[lo + 1];
     reinterpret_cast<int4*>(o)[0] = make_int4(start, end, lo, rec[1]);
-    reinterpret_cast<int4*>(o)[1] = make_int4(prefix[lo], prefix[lo + 1], rec[4], rec[5]);
+    reinterpret_cast<int4*>(o)[1] = make_int4(lo0, hi0, rec[4], rec[5]);
+    // the first page ids of the CTA's piece of that tile (padded with the last)
+    const int32_t* trow = tables + (int64_t)rec[1] * tstride;
+    const int p0 = start - lo0, n = (end < hi0 ? end : hi0) - lo0 - p0;
+    for (int k = 0; k < kPlanIds; ++k) o[8 + k] = trow[p0 + (k < n ? k : n - 1)];
   }
 }
 
@@ -198,10 +205,13 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
   // per-step plan (tim_attn_plan): this CTA's first tile, read in the same
   // round trip as the header instead of searched for afterwards
   int4 ph = make_int4(0, 0, 0, 0), pa = ph, pb = ph;
+  int32_t pid = 0;                           // lane's page id among the first kPlanIds of the range
   if (plan && !list) {
+    const int32_t* rec = plan + 8 + kPlanRec * cta;
     ph = __ldg(reinterpret_cast<const int4*>(plan));
-    pa = __ldg(reinterpret_cast<const int4*>(plan) + 2 + 2 * cta);
-    pb = __ldg(reinterpret_cast<const int4*>(plan) + 3 + 2 * cta);
+    pa = __ldg(reinterpret_cast<const int4*>(rec));
+    pb = __ldg(reinterpret_cast<const int4*>(rec) + 1);
+    pid = __ldg(rec + 8 + (threadIdx.x & 31));
   }
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
   const int n_dec = list ? hd.n_ext : hd.n_dec;
@@ -294,6 +304,34 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
       trace[8 * blockIdx.x + 4] = gtimer();
     }
     if (more) fetch();
+    // Planned CTAs issue their first two stages straight from the plan's page
+    // ids (one per lane), a round trip before the chunk's own id load lands.
+    int pre = 0;                                  // keys of the first chunk already issued
+    if (planned && more) {
+      const int navail = (p1 - c0) < kPlanIds ? (p1 - c0) : kPlanIds;
+      for (int k0 = 0; k0 < navail; k0 += C::TK, ++it) {
+        const int ntok = (navail - k0) < C::TK ? (navail - k0) : C::TK;
+        const int stg = it % C::STAGES;
+        if (it >= C::STAGES) mbar_wait(&empty[stg], ((it / C::STAGES) & 1) ^ 1);
+        if (!waited && c0 + k0 + ntok > fresh_cur) {
+          griddep_wait();
+          waited = true;
+        }
+        const int row = lane & (C::TK - 1);
+        const int32_t page = __shfl_sync(0xffffffffu, pid, k0 + (row < ntok ? row : ntok - 1));
+#ifdef TIM_CONSUMER_ONLY
+        if (lane == 0) mbar_arrive(&full[stg]);
+        (void)page;
+#else
+        if (lane == 0) mbar_arrive_expect_tx(&full[stg], 2 * C::TK * C::ROW_BYTES);
+        __syncwarp();
+        uint8_t* base = smem + stg * C::STAGE_BYTES + (lane >= C::TK ? C::TK * C::ROW_STRIDE : 0);
+        const __nv_bfloat16* src = (lane >= C::TK ? vl : kl) + (int64_t)page * (HKV * D) + (int64_t)hgrp_cur * HG * D;
+        bulk_g2s(base + row * C::ROW_STRIDE, src, C::ROW_BYTES, &full[stg]);
+#endif
+        pre = k0 + ntok;
+      }
+    }
     bool first_chunk = true;
     while (more) {
       __syncwarp();
@@ -319,7 +357,7 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
         if (more) fetch();
         advanced = true;
       };
-      for (int k0 = cur_c0; k0 < cur_c1; k0 += C::TK, ++it) {
+      for (int k0 = cur_c0 + (first_chunk ? pre : 0); k0 < cur_c1; k0 += C::TK, ++it) {
         const int ntok = (cur_c1 - k0) < C::TK ? (cur_c1 - k0) : C::TK;
         const int stg = it % C::STAGES;
         if (it >= C::STAGES) mbar_wait(&empty[stg], ((it / C::STAGES) & 1) ^ 1);
@@ -849,10 +887,11 @@ extern "C" int64_t tim_decode_ws_floats(int32_t n_ctas, int32_t max_dec, int32_t
   return (int64_t)(n_ctas + max_dec) * 8 * 16 * (head_dim + 2) + kPlanInts;
 }
 
-extern "C" int32_t tim_attn_plan(const int32_t* step, int32_t n_ctas, int32_t max_dec, int32_t head_dim,
-                                 float* ws, void* stream) {
+extern "C" int32_t tim_attn_plan(const int32_t* step, const int32_t* block_tables, int64_t table_stride,
+                                 int32_t n_ctas, int32_t max_dec, int32_t head_dim, float* ws, void* stream) {
   if (n_ctas <= 0 || n_ctas > kPlanMaxCtas) return TIM_OK;   // K1 falls back to its own search
-  attn_plan_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(step, n_ctas, max_dec, head_dim, ws);
+  attn_plan_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(step, block_tables, table_stride, n_ctas, max_dec,
+                                                        head_dim, ws);
   return check_launch("attn_plan");
 }
 

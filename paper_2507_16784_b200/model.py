@@ -552,7 +552,8 @@ class B200Transformer:
         dm = cfg.model_dim
         h = rt.h[:T]
         if self.tensor_cores:   # decode-tile partition of this step, shared by all layers
-            L.call("tim_attn_plan", sp, rt.n_ctas, rt.max_dec, cfg.head_dim, rt.ws.data_ptr(), st)
+            L.call("tim_attn_plan", sp, rt.tables.data_ptr(), rt.tables.shape[1], rt.n_ctas, rt.max_dec,
+                   cfg.head_dim, rt.ws.data_ptr(), st)
         L.call("tim_embed", rt.row_tokens.data_ptr(), T, self.emb.data_ptr(), dm, h.data_ptr(), td, st)
         return (2 if self.tensor_cores else 1) + self._layer_head(rt, 0, T)
 

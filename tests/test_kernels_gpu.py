@@ -75,7 +75,7 @@ def test_decode_bf16_matches_oracle(n_ctas, hq, hkv, planned):
     ctas = sms if n_ctas is None else n_ctas
     ws = torch.zeros(L.load().tim_decode_ws_floats(ctas, len(lengths), hkv, d), device="cuda")
     if planned:
-        L.call("tim_attn_plan", _ptr(step), ctas, len(lengths), d, _ptr(ws), _stream())
+        L.call("tim_attn_plan", _ptr(step), _ptr(_dev(tab)), stride, ctas, len(lengths), d, _ptr(ws), _stream())
     cnt = torch.zeros(len(lengths) * 8, device="cuda", dtype=torch.int32)
     tab_d = _dev(tab)
     for _ in range(2):  # twice: counters must self-reset

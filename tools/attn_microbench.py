@@ -58,7 +58,7 @@ def main():
     cnt = torch.zeros(a.batch * 8, dtype=torch.int32, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
     if not a.no_plan:   # the per-step plan the engine computes once per step
-        L.call("tim_attn_plan", step.data_ptr(), ctas, a.batch, d, ws.data_ptr(), st)
+        L.call("tim_attn_plan", step.data_ptr(), tab_d.data_ptr(), stride, ctas, a.batch, d, ws.data_ptr(), st)
 
     def run(l):
         L.call("tim_attn_decode", step.data_ptr(), 0, q.data_ptr(), out.data_ptr(), K[l].data_ptr(),

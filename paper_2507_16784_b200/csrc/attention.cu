@@ -47,8 +47,8 @@ struct AttnCfg {
   static constexpr int STAGE_BYTES = 2 * TK * ROW_STRIDE;
   static constexpr int STAGES_RAW = 204800 / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
-  static constexpr int THREADS = (NW + 1) * 32;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 16 + kIdChunk * 4;
+  static constexpr int THREADS = (NW + 2) * 32;        // consumers, producer, publisher
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 16 + kIdChunk * 4 + 16 + 4 * NW + 16;
   static constexpr int KC = D / 16;
   static constexpr int NT = D / 8;
 };
@@ -199,6 +199,9 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
   int32_t* s_ids = reinterpret_cast<int32_t*>(empty + C::STAGES);
+  uint64_t* pub_bar = reinterpret_cast<uint64_t*>(s_ids + kIdChunk);   // consumers -> publisher
+  uint64_t* pub_ack = pub_bar + 1;                                      // publisher read the round
+  int32_t* pub_tile = reinterpret_cast<int32_t*>(pub_ack + 1);         // [NW] tile to publish / -1 / -2
 
   unsigned long long* trace = g_trace;
   if (trace && threadIdx.x == 0) trace[8 * blockIdx.x] = gtimer();
@@ -235,6 +238,8 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
       mbar_init(&full[s2], 1);
       mbar_init(&empty[s2], NW);
     }
+    mbar_init(pub_bar, NW);
+    mbar_init(pub_ack, 1);
     fence_mbar_init();
   }
   // plan record: pa = {start, end, r0, slot0}, pb = {lo0, hi0, fresh0, hgrp0}
@@ -244,7 +249,25 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
   TileLane tl;
   tl.load(prefix, dec, n_dec, r0, lane);
   __syncthreads();
-  if (warp > NW) return;   // spare warps of a wider (one-launch) CTA
+  if (warp > NW + 1) return;   // spare warps of a wider (one-launch) CTA
+
+  if (warp == NW + 1) {
+    // ------------------------------------------------------------ publisher
+    // Bumps the K6 counters of this CTA's parked partials as soon as the
+    // consumer warps hand them over (their stores ordered by the CTA barrier
+    // and this warp's gpu-scope release), so a merger in another CTA is not
+    // kept waiting for this CTA's stream to end, and no consumer stalls on a
+    // release fence.
+    for (int round = 0;; ++round) {
+      mbar_wait(pub_bar, round & 1);
+      const int tile = lane < NW ? pub_tile[lane] : -1;
+      __syncwarp();
+      if (__all_sync(0xffffffffu, tile == -2 || lane >= NW)) break;
+      if (lane == 0) mbar_arrive(pub_ack);   // slots may be rewritten
+      if (tile >= 0) red_add_release(counters + (int64_t)tile * 8 + lane);
+    }
+    return;
+  }
 
   if (warp == NW) {
     // ------------------------------------------------------------ producer
@@ -409,8 +432,18 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
   float* ws_o = ws;
   float* ws_ml = ws + (int64_t)(grid + max_dec) * slot_floats;
   int it = 0, rb = r0;
-  int pend0 = -1, pend1 = -1;   // tiles this warp left partials for
-  bool sent0 = false;           // pend0 already signalled
+  int pub_round = 0;
+  // hand a parked partial's tile (-1: none in this warp, -2: stream done) to
+  // the publisher; every consumer warp takes part in every round
+  auto publish = [&](int tile) {
+    if (pub_round > 0) mbar_wait(pub_ack, (pub_round - 1) & 1);   // previous round read
+    __syncwarp();
+    if (lane == 0) {
+      pub_tile[warp] = tile;
+      mbar_arrive(pub_bar);
+    }
+    ++pub_round;
+  };
 
   // q fragments of a tile for this warp (the A operand of S = Q K^T).  The
   // next tile's fragments are fetched into the same registers as soon as the
@@ -571,9 +604,8 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
       l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 2);
     }
     const int cf = (int)cta_of(lo, G, N), cl = (int)cta_of(hi - 1, G, N);
-    if (cf != cl && nrows > 0 && c != cf) {
-      // non-merger piece: park the partial, signal after the stream
-      if (pend0 < 0) pend0 = r; else pend1 = r;
+    if (cf != cl && c != cf) {
+      // non-merger piece: park the partial and hand it to the publisher warp
       const int64_t wslot = ((int64_t)(c + r) * 8 + warp) * 16;   // first of this warp's 16 partial rows
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -586,14 +618,11 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
           if (t == 0) __stcg(reinterpret_cast<float2*>(ws_ml + (wslot + rr) * 2), make_float2(m_r[h], l_r[h]));
         }
       }
+      publish(nrows > 0 ? r : -1);
       continue;
     }
     if (cf != cl && nrows > 0) {
-      // merger (this CTA's last segment).  Publish this warp's earlier piece
-      // first (its stores drained long ago), so no CTA ever waits on a CTA
-      // that is itself waiting.
-      if (pend0 >= 0 && !sent0 && lane == 0) red_add_release(counters + (int64_t)pend0 * 8 + warp);
-      sent0 = true;
+      // merger (this CTA's last segment): wait for the other pieces
       int32_t* cnt = counters + (int64_t)r * 8 + warp;
       if (lane == 0) {
         while (ld_acquire(cnt) < cl - cf) {
@@ -639,11 +668,7 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
       }
     }
   }
-  // publish the pieces not yet signalled (release: orders their partial stores)
-  if (lane == 0) {
-    if (pend0 >= 0 && !sent0) red_add_release(counters + (int64_t)pend0 * 8 + warp);
-    if (pend1 >= 0) red_add_release(counters + (int64_t)pend1 * 8 + warp);
-  }
+  publish(-2);   // the publisher warp may retire
   if (trace && threadIdx.x == 0) trace[8 * blockIdx.x + 3] = gtimer();
 }
 

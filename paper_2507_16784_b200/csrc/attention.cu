@@ -203,10 +203,11 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
   uint64_t* pub_ack = pub_bar + 1;                                      // publisher read the round
   int32_t* pub_tile = reinterpret_cast<int32_t*>(pub_ack + 1);         // [NW] tile to publish / -1 / -2
 
-  unsigned long long* trace = g_trace;
-  if (trace && threadIdx.x == 0) trace[8 * blockIdx.x] = gtimer();
+  const unsigned long long t_start = gtimer();
   // per-step plan (tim_attn_plan): this CTA's first tile, read in the same
-  // round trip as the header instead of searched for afterwards
+  // round trip as the header instead of searched for afterwards (issued
+  // before anything else, the diagnostics pointer included, so the first
+  // copies are one round trip away)
   int4 ph = make_int4(0, 0, 0, 0), pa = ph, pb = ph;
   int32_t pid = 0;                           // lane's page id among the first kPlanIds of the range
   if (plan && !list) {
@@ -217,6 +218,8 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
     pid = __ldg(rec + 8 + (threadIdx.x & 31));
   }
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
+  unsigned long long* trace = g_trace;
+  if (trace && threadIdx.x == 0) trace[8 * blockIdx.x] = t_start;
   const int n_dec = list ? hd.n_ext : hd.n_dec;
   const int N = list ? hd.ext_total : hd.dec_total;
   const int want = (N + kMinTokensPerCta - 1) / kMinTokensPerCta;
@@ -624,14 +627,15 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
     if (cf != cl && nrows > 0) {
       // merger (this CTA's last segment): wait for the other pieces
       int32_t* cnt = counters + (int64_t)r * 8 + warp;
+      // Lane 0 acquires the count; the warp barrier orders the other lanes'
+      // partial loads after it (they read through L2, .cg, where the
+      // publishers' released stores live), saving a second round trip.
       if (lane == 0) {
         while (ld_acquire(cnt) < cl - cf) {
         }
+        *cnt = 0;   // re-arm for the next launch
       }
       __syncwarp();
-      (void)ld_acquire(cnt);   // every lane acquires the published partials
-      __syncwarp();
-      if (lane == 0) *cnt = 0;   // re-arm for the next launch
       for (int p = cf + 1; p <= cl; ++p) {
         const int64_t wslot = ((int64_t)(p + r) * 8 + warp) * 16;
 #pragma unroll

@@ -7,6 +7,7 @@ is raised.  Error codes map onto the reference exception types.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
@@ -79,7 +80,7 @@ def load(path: Path | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("TIMRUN_LIB") or LIB_PATH)   # TIMRUN_LIB: diagnostics builds
     if not p.exists():
         raise RuntimeError(
             f"libtimrun.so not found at {p}; build it with `python -m paper_2507_16784_b200.build` "

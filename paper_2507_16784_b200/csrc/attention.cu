@@ -38,6 +38,9 @@ constexpr int kMinTokensPerCta = 64;  // below this many kv tokens per CTA, use 
 // Decode tiles use HG = Hkv, WPH = 1 (one query x all heads, whole 2 KiB page
 // rows); multi-token tiles use fewer heads and more warps per head so one
 // K/V stream serves WPH x 16/group queries.
+#ifndef TIM_RING_BYTES
+#define TIM_RING_BYTES 204800   // shared-memory budget of the K/V ring
+#endif
 template <int D, int HG, int WPH>
 struct AttnCfg {
   static constexpr int NW = HG * WPH;                 // consumer warps
@@ -45,7 +48,7 @@ struct AttnCfg {
   static constexpr int ROW_BYTES = HG * D * 2;        // page-row slice per token and layer
   static constexpr int ROW_STRIDE = ROW_BYTES + 16;   // +16B: conflict-free ldmatrix rows
   static constexpr int STAGE_BYTES = 2 * TK * ROW_STRIDE;
-  static constexpr int STAGES_RAW = 204800 / STAGE_BYTES;
+  static constexpr int STAGES_RAW = TIM_RING_BYTES / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
   static constexpr int THREADS = (NW + 2) * 32;        // consumers, producer, publisher
   static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 16 + kIdChunk * 4 + 16 + 4 * NW + 16;
@@ -54,7 +57,7 @@ struct AttnCfg {
 };
 
 // Optional per-CTA timeline (%globaltimer, ns): [start, first data, loop end,
-// end, producer stamps] for CTA c at g_trace[8c..8c+6]; enabled by tim_set_trace (diagnostics).
+// end, producer stamps, last K6 release, merger count complete] for CTA c at g_trace[8c..8c+7]; enabled by tim_set_trace (diagnostics).
 __device__ unsigned long long* g_trace = nullptr;
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -116,6 +119,7 @@ struct TileLane {
 TIM_DEV void red_add_release(int32_t* p) {
   asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p) : "memory");
 }
+TIM_DEV void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 TIM_DEV int ld_acquire(const int32_t* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -249,8 +253,6 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
   const bool planned = plan && !list && hd.serial != 0 && ph.x == hd.serial && ph.y == G && ph.z == N &&
                        pa.x == start;
   const int r0 = planned ? pa.z : seg_search(prefix, n_dec, start, lane);   // first tile of this CTA
-  TileLane tl;
-  tl.load(prefix, dec, n_dec, r0, lane);
   __syncthreads();
   if (warp > NW + 1) return;   // spare warps of a wider (one-launch) CTA
 
@@ -268,9 +270,17 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
       if (__all_sync(0xffffffffu, tile == -2 || lane >= NW)) break;
       if (lane == 0) mbar_arrive(pub_ack);   // slots may be rewritten
       if (tile >= 0) red_add_release(counters + (int64_t)tile * 8 + lane);
+      if (trace && __any_sync(0xffffffffu, tile >= 0)) {
+        __syncwarp();
+        if (lane == 0) trace[8 * blockIdx.x + 6] = gtimer();   // last release issued
+      }
     }
     return;
   }
+  // The tile batch is loaded after the barrier: a planned producer issues its
+  // first copies from the plan alone, one round trip after the launch.
+  TileLane tl;
+  tl.load(prefix, dec, n_dec, r0, lane);
 
   if (warp == NW) {
     // ------------------------------------------------------------ producer
@@ -278,6 +288,7 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
     // page ids of chunk k+1 are loaded into registers while chunk k streams,
     // so neither a chunk nor a tile switch puts an id round trip between
     // two stages; each stage is then 2*TK bulk copies of whole page rows.
+    const uint64_t pol = l2_evict_first_policy();
     constexpr int IPL = kIdChunk / 32;     // ids per lane
     int32_t idr[IPL];
     int it = 0, rb = r0;
@@ -353,7 +364,7 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
         __syncwarp();
         uint8_t* base = smem + stg * C::STAGE_BYTES + (lane >= C::TK ? C::TK * C::ROW_STRIDE : 0);
         const __nv_bfloat16* src = (lane >= C::TK ? vl : kl) + (int64_t)page * (HKV * D) + (int64_t)hgrp_cur * HG * D;
-        bulk_g2s(base + row * C::ROW_STRIDE, src, C::ROW_BYTES, &full[stg]);
+        bulk_g2s_hint(base + row * C::ROW_STRIDE, src, C::ROW_BYTES, &full[stg], pol);
 #endif
         pre = k0 + ntok;
       }
@@ -405,8 +416,7 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
         const int32_t page = s_ids[k0 - cur_c0 + (row < ntok ? row : ntok - 1)];  // pad rows repeat a valid row
         uint8_t* base = smem + stg * C::STAGE_BYTES + (lane >= C::TK ? C::TK * C::ROW_STRIDE : 0);
         const __nv_bfloat16* src = (lane >= C::TK ? vl : kl) + (int64_t)page * (HKV * D) + hoff;
-        bulk_g2s(base + row * C::ROW_STRIDE, src, C::ROW_BYTES, &full[stg]);
-        if (trace && first_chunk && lane == 0 && k0 == cur_c0) trace[8 * blockIdx.x + 6] = gtimer();
+        bulk_g2s_hint(base + row * C::ROW_STRIDE, src, C::ROW_BYTES, &full[stg], pol);
         if (!advanced) {
           __syncwarp();   // the copies read s_ids: fetch() only fills registers, s_ids is rewritten next chunk
           advance();
@@ -627,6 +637,20 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
     if (cf != cl && nrows > 0) {
       // merger (this CTA's last segment): wait for the other pieces
       int32_t* cnt = counters + (int64_t)r * 8 + warp;
+      // Pull the other pieces' partials toward L2 while waiting: they were
+      // parked up to a whole launch earlier and are mostly evicted by the
+      // stream by now, and the merge below sits on the kernel's tail (L2 is
+      // the coherence point, so fetching a line before its final write is
+      // harmless).
+      for (int p = cf + 1; p <= cl; ++p) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (!valid[h]) continue;
+          const int64_t wrow = ((int64_t)(p + r) * 8 + warp) * 16 + g + 8 * h;
+          prefetch_l2(ws_o + wrow * D + 32 * t);
+          if (t == 0) prefetch_l2(ws_ml + wrow * 2);
+        }
+      }
       // Lane 0 acquires the count; the warp barrier orders the other lanes'
       // partial loads after it (they read through L2, .cg, where the
       // publishers' released stores live), saving a second round trip.
@@ -634,16 +658,17 @@ TIM_DEV void tiles_body(const int32_t* __restrict__ step, int list, const __nv_b
         while (ld_acquire(cnt) < cl - cf) {
         }
         *cnt = 0;   // re-arm for the next launch
+        if (trace && warp == 0) trace[8 * blockIdx.x + 7] = gtimer();   // merger's count complete
       }
       __syncwarp();
-      for (int p = cf + 1; p <= cl; ++p) {
-        const int64_t wslot = ((int64_t)(p + r) * 8 + warp) * 16;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int rr = g + 8 * h;
-          if (!valid[h]) continue;
-          const float2 ml = __ldcg(reinterpret_cast<const float2*>(ws_ml + (wslot + rr) * 2));
-          const float* ob = ws_o + (wslot + rr) * D;
+      for (int h = 0; h < 2; ++h) {
+        const int rr = g + 8 * h;
+        if (!valid[h]) continue;
+        for (int p = cf + 1; p <= cl; ++p) {
+          const int64_t wrow = ((int64_t)(p + r) * 8 + warp) * 16 + rr;
+          const float2 ml = __ldcg(reinterpret_cast<const float2*>(ws_ml + wrow * 2));
+          const float* ob = ws_o + wrow * D;
           float2 op[C::NT];
 #pragma unroll
           for (int j = 0; j < C::NT; ++j) op[j] = __ldcg(reinterpret_cast<const float2*>(ob + j * 8 + 2 * t));

@@ -95,12 +95,12 @@ def main():
         run(0)
         torch.cuda.synchronize()
         L.call("tim_set_trace", None)
-        t = tr.view(-1, 8).cpu().numpy().astype(np.float64)[:, :7]
+        t = tr.view(-1, 8).cpu().numpy().astype(np.float64)
         t0 = t[:, 0].min()
-        t = (t - t0) / 1000.0
-        print(json.dumps({k: [round(float(np.percentile(t[:, i], p)), 2) for p in (0, 50, 100)]
+        t = np.where(t > 0, (t - t0) / 1000.0, np.nan)   # unstamped slots -> nan
+        print(json.dumps({k: [round(float(np.nanpercentile(t[:, i], p)), 2) if np.isfinite(t[:, i]).any() else None for p in (0, 50, 100)]
                           for i, k in enumerate(["start", "first", "loop_end", "end", "p_tile", "p_ids",
-                                                 "p_issue"])}))
+                                                 "pub_rel", "merge_ok"])}))
         if a.dump:
             pre = np.concatenate([[0], np.cumsum(lens)])
             N = int(pre[-1])

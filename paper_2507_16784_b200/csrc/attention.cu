@@ -751,9 +751,14 @@ __global__ void __launch_bounds__(step_threads<D, HKV>(), 1)
   if (c < g0)
     tiles_body<D, HKV, HKV, 1>(step, 0, q, out, kl, vl, tables, tstride, hq, scale, ws, counters, max_dec, c, g0,
                                plan_of(ws, gridDim.x, max_dec, D));
-  else if (c < g0 + g1)
+  else if (c < g0 + g1) {
+    const unsigned long long t0 = gtimer();
     ext_tc_body(kl, vl, step, q, out, tables, tstride, hq, HKV, scale * kLog2e, c - g0, g1);
-  else
+    if (g_trace && threadIdx.x == 0) {   // diagnostics: K2 CTA start / end in the K1 slot layout
+      g_trace[8 * c] = t0;
+      g_trace[8 * c + 3] = gtimer();
+    }
+  } else
     griddep_wait();
 }
 

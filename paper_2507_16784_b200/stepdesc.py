@@ -62,13 +62,16 @@ class StepDesc:
 
     # Cost model of the one-launch attention (mode 2), in SM-microseconds,
     # calibrated on B200 with tools/attn_mixed_bench.py (mode 2, decode CTAs
-    # streaming next to the items): a decode-tile CTA streams ~40 KB/us of
-    # page rows; a multi-token item costs ~4 us (Q load, epilogue) plus ~1.6 us
-    # per 64-key block for each of its (up to two) 32-query blocks; items are
-    # dealt longest-first, round-robin.  TIMRUN_EXT_COST="item,block" overrides.
+    # streaming next to the items) and bench.py's mixed steps: a decode-tile
+    # CTA streams ~40 KB/us of page rows; a multi-token item costs ~3 us (Q
+    # load, epilogue) plus ~1.2 us per 64-key block for each of its (up to two)
+    # 32-query blocks; items are dealt longest-first, round-robin.  (4.0/1.6
+    # over-reserved CTAs for the items: bench mixed launches 66.1 -> 59.6 us;
+    # 2.0/0.8 under-reserves them: 68.7 us.)  TIMRUN_EXT_COST="item,block"
+    # overrides.
     DEC_US_PER_TOKEN = 4096 / 40e3
     EXT_US_PER_ITEM, EXT_US_PER_QBLOCK_BLOCK = (
-        float(x) for x in os.environ.get("TIMRUN_EXT_COST", "4.0,1.6").split(","))
+        float(x) for x in os.environ.get("TIMRUN_EXT_COST", "3.0,1.2").split(","))
 
     def attention_split(self) -> tuple[int, int]:
         """CTAs given to the decode tiles and to the multi-token items when

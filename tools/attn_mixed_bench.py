@@ -100,6 +100,19 @@ def main():
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) * 1000 / a.layers)
         us = float(np.median(times))
+        if a.trace and variant == "mode2":
+            ctas = L.load().tim_sm_count()
+            tr = torch.zeros(ctas * 8, dtype=torch.int64, device="cuda")
+            L.call("tim_set_trace", tr.data_ptr())
+            run(0)
+            torch.cuda.synchronize()
+            L.call("tim_set_trace", None)
+            t = tr.view(ctas, 8).cpu().numpy().astype(np.float64)
+            t0 = t[:, 0][t[:, 0] > 0].min()
+            dec, ext = t[:split[0]], t[split[0]:split[0] + split[1]]
+            pct = lambda x: [round(float(np.percentile((x - t0) / 1000, p)), 2) for p in (0, 50, 90, 100)]
+            print(json.dumps({"dec_end": pct(dec[:, 3]), "dec_loop_end": pct(dec[:, 2]), "ext_end": pct(ext[:, 3])}),
+                  file=sys.stderr)
         if a.trace and sd.ext:
             tr = torch.zeros(64 * 8, dtype=torch.int64, device="cuda")
             L.call("tim_tc_trace", tr.data_ptr())

@@ -194,8 +194,13 @@ def run_gpu(args, rank: int, world: int, dist):
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    prof = os.environ.get("TIMRUN_PROFILE_TIMED") == "1"   # ncu --profile-from-start off: launch list of the value window
     e0.record()
+    if prof:
+        torch.cuda.profiler.start()
     rt.replay(resident)
+    if prof:
+        torch.cuda.profiler.stop()
     e1.record()
     barrier()
     clk = clocks.stop()

@@ -2,6 +2,7 @@
 into per-kernel share of the step: python tools/launch_summary.py file.csv"""
 import collections
 import csv
+import gzip
 import re
 import sys
 
@@ -16,7 +17,8 @@ def short(name: str) -> str:
 
 
 def main(path):
-    rows = [r for r in csv.reader(line for line in open(path) if line.startswith('"'))]
+    opener = gzip.open if path.endswith(".gz") else open
+    rows = [r for r in csv.reader(line for line in opener(path, "rt") if line.startswith('"'))]
     h = rows[0]
     ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
     per = collections.defaultdict(dict)

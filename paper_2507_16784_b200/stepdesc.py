@@ -73,6 +73,23 @@ class StepDesc:
     EXT_US_PER_ITEM, EXT_US_PER_QBLOCK_BLOCK = (
         float(x) for x in os.environ.get("TIMRUN_EXT_COST", "3.0,1.2").split(","))
 
+    def _split_cost(self, ext: list) -> tuple[float, int]:
+        """(estimated us, CTAs for the items) of the best split for `ext`."""
+        G = self.ctas
+        times = sorted((self.EXT_US_PER_ITEM + self.EXT_US_PER_QBLOCK_BLOCK * ((e[3] + 31) // 32)
+                        * ((e[2] + 63) // 64) for e in ext), reverse=True)
+        n = len(times)
+        if not self.dec:
+            return (sum(times[0::min(G, n)]), G)
+        w0 = sum(d[2] for d in self.dec) * self.DEC_US_PER_TOKEN
+        best, best_g1 = None, 1
+        for g1 in range(1, min(G - 1, n) + 1):
+            t1 = sum(times[0::g1])          # CTA 0's items (longest first, round-robin)
+            t = max(w0 / (G - g1), t1)
+            if best is None or t < best:
+                best, best_g1 = t, g1
+        return (best, best_g1)
+
     def attention_split(self) -> tuple[int, int]:
         """CTAs given to the decode tiles and to the multi-token items when
         both run in one launch: minimise the slower side's estimated time."""
@@ -81,17 +98,41 @@ class StepDesc:
             return (G, 0)
         if not self.dec:
             return (0, G)
-        w0 = sum(d[2] for d in self.dec) * self.DEC_US_PER_TOKEN
-        times = sorted((self.EXT_US_PER_ITEM + self.EXT_US_PER_QBLOCK_BLOCK * ((e[3] + 31) // 32)
-                        * ((e[2] + 63) // 64) for e in self.ext), reverse=True)
-        n = len(times)
-        best, best_g1 = None, 1
-        for g1 in range(1, min(G - 1, n) + 1):
-            t1 = sum(times[0::g1])          # CTA 0's items (longest first, round-robin)
-            t = max(w0 / (G - g1), t1)
-            if best is None or t < best:
-                best, best_g1 = t, g1
-        return (G - best_g1, best_g1)
+        g1 = self._split_cost(self.ext)[1]
+        return (G - g1, g1)
+
+    @staticmethod
+    def halve_items(ext: list) -> list:
+        """Each item of > 32 queries as two items of <= 32 (the kernel skips a
+        32-query item's second MMA tile): the K/V slice is streamed twice, but
+        the work comes in half-size pieces."""
+        out = []
+        for row, slot, kv_len, nq, fresh, grp in ext:
+            if nq <= 32:
+                out.append((row, slot, kv_len, nq, fresh, grp))
+            else:
+                out.append((row, slot, kv_len - (nq - 32), 32, fresh, grp))
+                out.append((row + 32, slot, kv_len, nq - 32, fresh, grp))
+        return out
+
+    def choose_item_size(self) -> None:
+        """Whole items (two MMA tiles sharing each K/V block) are the cheaper
+        work per query; halves only pay when SMs would otherwise idle: a step
+        with no decode rows (prefill / extend only) and fewer items than half
+        the CTAs.  (Halving against the mode-2 split as well, whenever the
+        cost model predicted a gain, measured 62.9 -> 62.2 us and 78.9 -> 75.0
+        us in tools/attn_mixed_bench.py but 61.2 -> 62.0 us on the bench's
+        mixed steps, so mixed steps keep whole items.)  TIMRUN_HALVE_ITEMS=0
+        disables, =2 also halves in mixed steps when the model predicts a gain."""
+        mode = os.environ.get("TIMRUN_HALVE_ITEMS", "1")
+        if mode == "0" or self.ctas <= 0 or not self.ext or all(e[3] <= 32 for e in self.ext):
+            return
+        halves = self.halve_items(self.ext)
+        if not self.dec:
+            if 2 * len(self.ext) <= self.ctas:
+                self.ext = halves
+        elif mode == "2" and self._split_cost(halves)[0] < 0.97 * self._split_cost(self.ext)[0]:
+            self.ext = halves
 
     # ---------------------------------------------------------------- pack
     def pack(self) -> np.ndarray:
@@ -122,6 +163,7 @@ class StepDesc:
         hdr["off_dec_prefix"] = off
         parts.append(prefix.astype(np.int32))
         off += prefix.size
+        self.choose_item_size()
         # longest items first: the kernel deals them round-robin to its CTAs
         self.ext.sort(key=lambda e: -e[2])
         add("ext", self.ext, L.EXT_FIELDS)

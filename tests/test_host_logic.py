@@ -188,11 +188,36 @@ def test_attention_split_cost_model():
 
 def test_pack_sorts_items_and_stamps_serial():
     sd = StepDesc()
-    sd.ext += [(0, 0, 100, 8, 92, 0), (0, 0, 700, 64, 636, 1), (0, 0, 300, 8, 292, 2)]
+    sd.ext += [(0, 0, 100, 8, 92, 0), (0, 0, 700, 40, 660, 1), (0, 0, 300, 8, 292, 2)]
     sd.serial, sd.ctas = 17, 148
     arr = sd.pack()
     hdr = {k: int(arr[i]) for i, k in enumerate(_HDR)}
-    assert hdr["serial"] == 17 and hdr["n_ext"] == 3
-    ext = arr[hdr["off_ext"]:hdr["off_ext"] + 3 * L.EXT_FIELDS].reshape(3, L.EXT_FIELDS)
-    assert ext[:, 2].tolist() == [700, 300, 100]       # longest first (round-robin dealing)
+    # extend-only step with few items: the 40-query item is halved (32 + 8)
+    assert hdr["serial"] == 17 and hdr["n_ext"] == 4
+    ext = arr[hdr["off_ext"]:hdr["off_ext"] + 4 * L.EXT_FIELDS].reshape(4, L.EXT_FIELDS)
+    assert ext[:, 2].tolist() == [700, 692, 300, 100]   # longest first (round-robin dealing)
     assert hdr["split_dec_ctas"] == 0 and hdr["split_ext_ctas"] == 148
+
+
+def test_item_halving():
+    """A > 32-query item splits into rows [row, row+32) and [row+32, row+nq)
+    with the causal key counts of each half; whole items are kept in mixed
+    steps and in extend-only steps with enough items for the CTAs."""
+    halves = StepDesc.halve_items([(10, 3, 700, 64, 636, 5), (80, 3, 900, 20, 880, 2)])
+    assert halves == [(10, 3, 668, 32, 636, 5), (42, 3, 700, 32, 636, 5), (80, 3, 900, 20, 880, 2)]
+    for q in range(64):   # every query keeps its visible-key limit kv_len - nq + qi
+        row, kv, nq = (halves[0][0], 668, 32) if q < 32 else (halves[1][0], 700, 32)
+        assert kv - nq + (10 + q - row) == 700 - 64 + q
+
+    def run(n_items, with_dec):
+        sd = StepDesc()
+        sd.ctas = 148
+        sd.ext += [(0, 0, 700, 64, 636, h % 8) for h in range(n_items)]
+        if with_dec:
+            sd.dec += [(i, i, 700, 1, 699, 0) for i in range(64)]
+        sd.choose_item_size()
+        return len(sd.ext)
+
+    assert run(16, False) == 32         # idle SMs: halves
+    assert run(100, False) == 100       # enough items: whole
+    assert run(16, True) == 16          # mixed step: whole (default)

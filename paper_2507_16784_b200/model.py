@@ -175,6 +175,18 @@ class StepRuntime:
         self.attn_events = None      # list -> CUDA events around layer-0 decode attention
 
     # ----------------------------------------------------------- buffers
+    def grow_logical(self, n: int) -> None:
+        """Reallocate the per-slot token streams to hold n indices (doubling).
+        Only eager kernels (K4, row staging) read this buffer, so no captured
+        graph holds its address."""
+        cap = self.logical.shape[1]
+        if n <= cap:
+            return
+        new_cap = max(n, 2 * cap)
+        buf = torch.zeros((self.logical.shape[0], new_cap), dtype=torch.int32, device=self.dev)
+        buf[:, :cap] = self.logical
+        self.logical = buf
+
     def _ensure_rows(self, n: int) -> None:
         if n <= self._rows:
             return

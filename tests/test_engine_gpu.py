@@ -411,3 +411,60 @@ def test_run_until_done_and_deadline(golden):
     assert out[rid]["status"] == "finished"
     h = eng2.health()
     assert h["finished"] == 1 and h["pool"]["free"] == h["pool"]["capacity"]
+
+
+def test_unscripted_without_logits_fails_like_reference():
+    """scheduler.py:428-429: a backend that produces no logits fails an
+    unscripted request with ScriptError (never loops)."""
+    eng = _scripted(threshold=1)
+    a = eng.submit("p:")                 # prompt forwarded, but ScriptedModel has no logits
+    b = eng.submit("")                   # nothing to forward at all
+    for _ in range(3):
+        eng.step()
+    for rid in (a, b):
+        res = eng.result(rid)
+        assert res["status"] == "failed" and res["failure"].startswith("ScriptError"), res
+    assert eng.pool.free_count == eng.pool.capacity
+
+
+def test_tool_response_nesting_limit_follows_grammar_depth():
+    """scheduler.py:483-484: responses up to json_depth_limit-1 = 2*depth_limit-1
+    levels are kept; deeper ones are replaced by the error object."""
+    doc = '[{"thought":"ask","tool_name":"t","parameters":{},"tool_result":0,"conclusion":"done"}]'
+    trace = tr.make_trace_from_text(doc)
+
+    def nested(d):
+        v = 1
+        for _ in range(d - 1):
+            v = {"k": v}
+        return {"k": v}
+
+    for depth, kept in ((20, True), (31, True), (32, False)):
+        eng = _scripted(threshold=1)
+        rid = eng.submit("p:", [tr.ToolSpec("t")], script=trace.script,
+                         tool_responses={0: nested(depth)})
+        eng.run_until_done()
+        text = eng.result(rid)["text"]
+        assert ('"tool_result":{"k":' in text) is kept, (depth, text[:120])
+        assert ("exceeds nesting limit" in text) is (not kept)
+
+
+def test_logical_stream_grows_past_engine_cap():
+    """A per-request max_output_tokens above the engine's: the
+    device token stream grows instead of spilling into the next slot, and
+    both requests still finish bit-identically to their scripts."""
+    from paper_2507_16784_b200.traces import deep_recursion_doc
+    doc = deep_recursion_doc(8, 2, seed=0, text_chars=6)
+    trace = tr.make_trace_from_text(doc)
+    P = 512
+    eng = tr.Engine(tr.ScriptedModel(position_limit=P),
+                    tr.BatchConfig(buffer_threshold=1, position_limit=P, pool_pages=4 * P,
+                                   max_output_tokens=16, max_batch=2, check_device=True))
+    cap0 = eng.runtime.logical.shape[1]
+    assert len(trace.script) > cap0
+    rids = [eng.submit(f"w{i}:", script=trace.script, max_output_tokens=10 ** 6) for i in range(2)]
+    eng.run_until_done()
+    for rid in rids:
+        assert eng.result(rid)["status"] == "finished"
+        assert eng.result(rid)["text"] == doc
+    assert eng.runtime.logical.shape[1] > cap0

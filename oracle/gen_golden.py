@@ -282,6 +282,128 @@ def gen_corpus():
     dump("corpus_tool_chain32.json.gz", c2)
     c1 = [make_trace(random_tree(s, 3, 3, tool_prob=0.3), TOK).text for s in range(100)]
     dump("corpus_random_3_3.json.gz", c1)
+    # acceptance criterion 1 (tests/test_acceptance.py:40-53): verify.suite_prune_extend's trees
+    a1 = [make_trace(random_tree(s, 4, 2, tool_prob=0.25), TOK).text for s in range(100)]
+    dump("corpus_random_4_2_025.json.gz", a1)
+
+
+# ------------------------------------------------------------------------------
+# Bench-configuration runs (BASELINE configs 2-4): per-step checksums of the
+# reference Engine's paging state, in the definition of
+# paper_2507_16784_b200/checksum.py (restated here in numpy so the generator
+# does not depend on the product package).
+_MUL, _STRIDE = 2654435761, 7919
+
+
+def _w(idx):
+    idx = np.asarray(idx, dtype=np.int64)
+    return (((idx * _MUL) & 0xFFFFFFFF) >> 16) + 1
+
+
+def _seq_hash(values, k=0):
+    v = np.asarray(values, dtype=np.int64)
+    if v.size == 0:
+        return 0
+    return int(((v + 1) * _w(np.arange(v.size, dtype=np.int64) + _STRIDE * k)).sum())
+
+
+def _host_hash(live_lens, pending_lens, decoded):
+    h = 0
+    for rid, n in live_lens.items():
+        k = int(rid[1:])
+        h += (n + 1) * int(_w(3 * k)) + (pending_lens.get(rid, 0) + 1) * int(_w(3 * k + 1))
+    for rid, n in decoded.items():
+        k = int(rid[1:])
+        h += (n + 1) * int(_w(3 * k + 2))
+    return h & 0x7FFFFFFFFFFFFFFF
+
+
+BENCH_COLS = ["step", "active", "awaiting_tool", "finished", "failed", "pages_free", "flops_units",
+              "host_hash", "table_hash", "live_hash", "free_hash"]
+
+
+def run_bench_scenario(name, docs, prompts, cfg, position_limit, every=1):
+    """Reference scripted Engine over `docs`; one checksum row per `every` steps
+    (and the last step).  Returns (rows int64 [n, 11], meta)."""
+    engine = Engine(ScriptedModel(position_limit=position_limit), cfg)
+    rids = []
+    for doc, prompt in zip(docs, prompts):
+        tr = make_trace_from_doc(doc)
+        rids.append(engine.submit(prompt, [ToolSpec(n) for n in tr.tool_names], script=tr.script,
+                                  tool_responses=tr.tool_responses or None))
+    rows = []
+    while not engine.all_terminal():
+        rep = engine.step()
+        if rep.step % every and not engine.all_terminal():
+            continue
+        pend = {rid: len(engine.requests[rid].pending) for rid in rep.request_live}
+        th = lh = 0
+        for rid in rids:
+            r = engine.requests[rid]
+            k = int(rid[1:])
+            if r.table.pages:
+                th += _seq_hash(r.table.pages, k)
+                lh += _seq_hash(r.live, k)
+        rows.append([rep.step, rep.active, rep.awaiting_tool, rep.finished, rep.failed,
+                     rep.pages_free, rep.flops_units, _host_hash(rep.request_live, pend, rep.decoded),
+                     th, lh, _seq_hash(engine.pool.free_list)])
+    meta = {"name": name, "config": cfg.__dict__, "position_limit": position_limit, "every": every,
+            "prompts": prompts, "rids": rids, "n_steps": engine.step_index, "requests": {}}
+    for rid in rids:
+        r = engine.requests[rid]
+        meta["requests"][rid] = {
+            "status": r.status.value,
+            "metrics": r.metrics.to_dict(),
+            "evictions": len(r.eviction_log),
+            "eviction_hash": _seq_hash([x for s in r.eviction_log for x in (s.start, s.end)]),
+            "applied_hash": _seq_hash([x for s in r.applied_spans for x in (s.start, s.end)]),
+            "logical_hash": _seq_hash(r.logical),
+        }
+    return np.asarray(rows, dtype=np.int64), meta
+
+
+def make_trace_from_doc(doc):
+    from threadrun.schema import parse_tree_text
+    return make_trace(parse_tree_text(doc), TOK)
+
+
+def gen_bench():
+    """C2 (64 x tool_chain_tree(32), T=2, P=40960, pool 64x1600), C3 shards
+    (512 documents dealt round-robin over G GPUs) and a C4 slice (4 x
+    deep_recursion_tree(8,3,text_chars=16) after a 12,000-token prompt, P=16384,
+    to completion): exactly the engines bench.py / tools/bench_configs.py build."""
+    import time
+    chain = [make_trace(tool_chain_tree(32, seed=i), TOK).text for i in range(512)]
+    arrays, metas = {}, []
+
+    def c23(name, G, r):
+        idx = [i for i in range(64 * G) if i % G == r]
+        cfg = BatchConfig(max_batch=64, buffer_threshold=2, position_limit=40960, pool_pages=64 * 1600,
+                          max_queue=64, check_masks=False, max_output_tokens=20000)
+        t0 = time.time()
+        rows, meta = run_bench_scenario(name, [chain[i] for i in idx], [f"q{i}:" for i in idx], cfg, 40960)
+        meta["docs"] = idx
+        print(name, rows.shape, f"{time.time() - t0:.0f}s")
+        arrays[name] = rows
+        metas.append(meta)
+
+    c23("c2_g1_r0", 1, 0)
+    c23("c3_g8_r0", 8, 0)
+    c23("c3_g2_r1", 2, 1)
+    deep = [make_trace(deep_recursion_tree(8, 3, seed=i, text_chars=16), TOK).text for i in range(4)]
+    dump("corpus_deep8_3_16.json.gz", deep)
+    cfg = BatchConfig(max_batch=4, buffer_threshold=2, position_limit=16384, pool_pages=4 * 16384,
+                      max_queue=64, check_masks=False, max_output_tokens=140_000)
+    prompt = "a" * 12000
+    t0 = time.time()
+    rows, meta = run_bench_scenario("c4_slice", deep, [prompt] * 4, cfg, 16384, every=16)
+    meta["prompts"] = ["a*12000"] * 4
+    meta["docs"] = list(range(4))
+    print("c4_slice", rows.shape, f"{time.time() - t0:.0f}s")
+    arrays["c4_slice"] = rows
+    metas.append(meta)
+    np.savez_compressed(OUT / "bench_runs.npz", **arrays)
+    dump("bench_runs.json.gz", {"columns": BENCH_COLS, "scenarios": metas})
 
 
 if __name__ == "__main__":

@@ -23,6 +23,10 @@ from oracle import pruning as opr
 
 pytestmark = pytest.mark.gpu
 
+from pathlib import Path  # noqa: E402
+
+GOLDEN_DIR = Path(__file__).resolve().parent / "golden"
+
 
 def _load(golden, name):
     with gzip.open(golden / name, "rt", encoding="utf-8") as f:
@@ -172,7 +176,9 @@ def test_engine_numeric_replay_matches_reference(golden):
 
 
 def _kv_equivalence(eng, req, model, rtol, greedy_steps=8):
-    """verify.py:99-135 restated: working memory == fresh prefill of live tokens."""
+    """verify.py:99-135 restated: working memory == fresh prefill of the live
+    tokens (K, V at rtol), then the next `greedy_steps` unmasked greedy tokens
+    agree between the runtime's state and the fresh-prefill state."""
     live_tokens = [req.logical[i] for i in req.live]
     n = len(live_tokens)
     scratch = model.make_pool(n + greedy_steps + 2)
@@ -180,15 +186,29 @@ def _kv_equivalence(eng, req, model, rtol, greedy_steps=8):
     o_logits = model.prefill(live_tokens, list(range(n)), ot, scratch)
     kr, vr = tr.gather(eng.pool, req.table)
     ko, vo = tr.gather(scratch, ot)
-    assert _rel(kr, ko) < rtol and _rel(vr, vo) < rtol
-    return max(_rel(kr, ko), _rel(vr, vo))
+    k_rel, v_rel = _rel(kr, ko), _rel(vr, vo)
+    assert k_rel < rtol and v_rel < rtol, (k_rel, v_rel)
+    run_pool = model.make_pool(n + greedy_steps + 2)
+    rt_ = tr.PageTable("runtime")
+    rt_.pages = run_pool.alloc("runtime", n)
+    src = torch.tensor(req.table.pages, dtype=torch.long, device="cuda")
+    dst = torch.tensor(rt_.pages, dtype=torch.long, device="cuda")
+    run_pool.K_layers[:, dst] = eng.pool.K_layers[:, src]
+    run_pool.V_layers[:, dst] = eng.pool.V_layers[:, src]
+    l_run, l_ora = req.last_logits, o_logits
+    for _ in range(greedy_steps):
+        t_run, t_ora = int(np.argmax(l_run)), int(np.argmax(l_ora))
+        assert t_run == t_ora, f"greedy continuation diverged: {t_run} vs {t_ora}"
+        l_run = model.decode_step(t_run, len(rt_), rt_, run_pool)
+        l_ora = model.decode_step(t_ora, len(ot), ot, scratch)
+    return max(k_rel, v_rel)
 
 
 @pytest.mark.parametrize("threshold", [0, 1, 2])
 def test_prune_reencode_equals_fresh_prefill(golden, threshold):
-    """Acceptance criterion 1 (tests/test_acceptance.py:40-53) on the device:
-    after every eviction + re-encode the retained working memory equals a fresh
-    prefill of the pruned logical sequence at 1e-5 (fp32)."""
+    """Acceptance criterion 1 shape on the device (C1 dims): after every
+    eviction + re-encode the retained working memory equals a fresh prefill of
+    the pruned logical sequence at 1e-5 (fp32) and greedy decoding agrees."""
     recs = [r for r in _load(golden, "events.json.gz") if r["gen"][0] == "random_tree"][:25]
     model = tr.B200Transformer(tr.ModelConfig(**C1))
     checked = 0
@@ -207,6 +227,40 @@ def test_prune_reencode_equals_fresh_prefill(golden, threshold):
                 checked += 1
         assert eng.result(rid)["text"] == rec["text"]
     assert checked >= 10
+
+
+def test_acceptance_criterion_1_full():
+    """tests/test_acceptance.py:40-53 with verify.suite_prune_extend's exact
+    inputs (verify.py:139-163): random_tree(seed, 4, 2, tool_prob=0.25) for
+    seeds 0..99, T=0, ModelConfig(position_limit=2048), prompt "task:", tools
+    search/calc, pool 4*P, page-leak audit every step (verify.py:80-82), every
+    eviction checked at 1e-5 with the 8-step greedy continuation."""
+    from paper_2507_16784_b200.traces import load_corpus, make_trace_from_text
+    docs = load_corpus(GOLDEN_DIR / "corpus_random_4_2_025.json.gz")
+    assert len(docs) == 100
+    model = tr.B200Transformer(tr.ModelConfig(position_limit=2048))
+    checked, worst = 0, 0.0
+    for doc in docs:
+        t = make_trace_from_text(doc)
+        eng = tr.Engine(model, tr.BatchConfig(buffer_threshold=0, position_limit=2048,
+                                              pool_pages=4 * 2048))
+        rid = eng.submit("task:", [tr.ToolSpec("search"), tr.ToolSpec("calc")], script=t.script,
+                         tool_responses=t.tool_responses or None)
+        req = eng.requests[rid]
+        pruned = 0
+        while not eng.all_terminal():
+            eng.step()
+            live = sum(len(r.live) for r in eng.requests.values())
+            assert eng.pool.capacity - eng.pool.free_count == live, "page leak"
+            if req.metrics.pruned_tokens > pruned:
+                pruned = req.metrics.pruned_tokens
+                if req.status.value == "decoding":
+                    worst = max(worst, _kv_equivalence(eng, req, model, 1e-5))
+                    checked += 1
+        res = eng.result(rid)
+        assert res["status"] == "finished" and res["text"] == doc
+    assert checked >= 100 and worst < 1e-5
+    print(f"acceptance 1: 100 trees, {checked} evictions, worst rel err {worst:.2e}")
 
 
 def test_batched_engine_equals_sequential_oracle_bf16(golden):
@@ -249,7 +303,10 @@ def test_batched_engine_equals_sequential_oracle_bf16(golden):
             lo = oracle.prefill(toks, list(range(len(toks))), t, pool)
             ko, vo = op.gather(pool, t)
             kr, vr = tr.gather(eng.pool, req.table)
-            assert np.abs(kr - ko).max() < 0.1 and np.abs(vr - vo).max() < 0.1
+            # bf16 activations + KV vs the fp32 oracle end to end: the error is
+            # bf16 rounding of h / qkv (not attention, which the in-engine
+            # test holds to 2e-2 max-abs), so the bound is relative to max|ref|
+            assert _rel(kr, ko) <= 2e-2 and _rel(vr, vo) <= 2e-2, (_rel(kr, ko), _rel(vr, vo))
             assert np.abs(kr - ko).mean() < 5e-3
             checks += 1
     assert checks >= 6

@@ -57,8 +57,19 @@ def _tables(lengths, cap, stride, seed):
 @pytest.mark.parametrize("hq,hkv", [(32, 8), (16, 4), (8, 8), (32, 2)])
 def test_decode_bf16_matches_oracle(n_ctas, hq, hkv, planned):
     """Decode tiles (K1), with and without the per-step plan (tim_attn_plan)."""
+    _decode_case([1, 2, 15, 16, 17, 100, 777, 1500, 33, 4096], n_ctas, hq, hkv, planned)
+
+
+@pytest.mark.parametrize("planned", [False, True])
+@pytest.mark.parametrize("n_ctas", [None, 7])
+def test_decode_bf16_long_horizon_lengths(n_ctas, planned):
+    """C4 retained lengths (12K-token prompt + working memory, up to the 16,384
+    position limit) on the C2 head shape."""
+    _decode_case([13378, 16384, 12001, 3, 16383, 9000, 12500, 64], n_ctas, 32, 8, planned)
+
+
+def _decode_case(lengths, n_ctas, hq, hkv, planned):
     d = 128
-    lengths = [1, 2, 15, 16, 17, 100, 777, 1500, 33, 4096]
     cap = sum(lengths) + 7
     stride = max(lengths)
     kp, vp = _pool(cap, hkv, d, torch.bfloat16, 1)
@@ -112,14 +123,24 @@ def _extend_case(hq, hkv, d, dtype, segs_mn, seed):
     return kp, vp, tab, stride, q, sd, rows
 
 
+SEGSETS = {
+    "mixed": [(0, 1), (0, 7), (5, 33), (100, 64), (700, 150), (0, 200), (1200, 3), (40, 1)],
+    # C4: re-encodes / decode rows behind a 12K-16K retained prefix
+    "long": [(13000, 150), (12000, 1), (16000, 64), (9000, 33), (14000, 1), (5, 1)],
+}
+
+
+@pytest.mark.parametrize("segset", ["mixed", "long"])
 @pytest.mark.parametrize("one_launch", [False, True])
 @pytest.mark.parametrize("n_ctas", [None, 5])
 @pytest.mark.parametrize("hq,hkv", [(32, 8), (16, 4), (4, 4), (32, 2)])
-def test_extend_tiles_bf16_matches_oracle(hq, hkv, n_ctas, one_launch):
+def test_extend_tiles_bf16_matches_oracle(hq, hkv, n_ctas, one_launch, segset):
     """Multi-query tiles (re-encode / prefill / tool rows) through the unified
     split-K kernel: paged prefix fully visible + causal new block."""
+    if segset == "long" and (hq, hkv) != (32, 8):
+        pytest.skip("long prefixes only at the C2/C4 head shape")
     d = 128
-    segs = [(0, 1), (0, 7), (5, 33), (100, 64), (700, 150), (0, 200), (1200, 3), (40, 1)]
+    segs = SEGSETS[segset]
     kp, vp, tab, stride, q, sd, rows = _extend_case(hq, hkv, d, torch.bfloat16, segs, 11)
     qpi = L.load().tim_extend_queries_per_item(hq, hkv, d, L.DTYPE_BF16)
     ngr = L.load().tim_extend_head_groups(hq, hkv, d)

@@ -208,3 +208,51 @@ def test_gqa_reduces_to_reference_when_kv_equals_heads():
     b = om.init_weights(om.Config(layers=1, heads=4, head_dim=8, kv_heads=4, mlp_dim=128))
     for k in ("wq", "wk", "wv", "wo", "w1", "w2"):
         assert np.array_equal(a["layers"][0][k], b["layers"][0][k])
+
+
+def test_oracle_engine_matches_reference_bench_config(golden):
+    """The oracle engine pinned at the C2 bench configuration (64 x
+    tool_chain_tree(32), T=2, P=40960): the first 600 steps' reports and
+    table / live / free-list checksums equal the reference run's
+    (tests/golden/bench_runs.*, oracle/gen_golden.py gen_bench)."""
+    import gzip as _gz
+    import json as _json
+    from paper_2507_16784_b200.checksum import host_hash, seq_hash_np
+    from paper_2507_16784_b200.structure import StructureScanner
+    from paper_2507_16784_b200.traces import load_corpus, make_trace_from_text
+    with _gz.open(golden / "bench_runs.json.gz", "rt") as f:
+        meta = next(s for s in _json.load(f)["scenarios"] if s["name"] == "c2_g1_r0")
+    rows = np.load(golden / "bench_runs.npz")["c2_g1_r0"]
+    docs = load_corpus(golden / "corpus_tool_chain32.json.gz")
+    cfg = meta["config"]
+    tok = build_tokenizer()
+    eng = oe.Engine(oe.Accounting(40960), max_batch=64, threshold=cfg["buffer_threshold"],
+                    position_limit=40960, pool_pages=cfg["pool_pages"], max_queue=cfg["max_queue"],
+                    max_output_tokens=cfg["max_output_tokens"], tokenize=tok.tokenize)
+    for d, prompt in zip(meta["docs"], meta["prompts"]):
+        t = make_trace_from_text(docs[d])
+        sc, evs, stream, call = StructureScanner(tok), [], [], 0
+        for tid in t.script:
+            for e in sc.feed(tid):
+                evs.append([e.kind, len(stream), e.depth, e.payload])
+            stream.append(tid)
+            if any(e[0] == "ToolResultSlotOpened" and e[1] == len(stream) - 1 for e in evs[-3:]):
+                text = _json.dumps(t.tool_responses[call], separators=(",", ":"), ensure_ascii=False)
+                for rt_ in tok.tokenize(text):
+                    for e in sc.feed(rt_):
+                        evs.append([e.kind, len(stream), e.depth, e.payload])
+                    stream.append(rt_)
+                call += 1
+        eng.submit(tok.tokenize(prompt), t.script, t.tool_responses, oe.event_table(evs))
+    for g in rows[:600]:
+        rep = eng.step()
+        live = rep["request_live"]
+        pend = {rid: len(eng.requests[rid].pending) for rid in live}
+        th = lh = 0
+        for rid, r in eng.requests.items():
+            if r.table.pages:
+                th += seq_hash_np(r.table.pages, int(rid[1:]))
+                lh += seq_hash_np(r.live, int(rid[1:]))
+        mine = list(rep["report"]) + [host_hash(live, pend, rep["decoded"]), th, lh,
+                                      seq_hash_np(eng.pool.free_list)]
+        assert mine == [int(x) for x in g], (int(g[0]), mine, g.tolist())

@@ -2,29 +2,35 @@
 
 Workload (N=1 line = BASELINE config 2, C2): Qwen3-8B-shaped TIM decoder
 (36 layers, hidden 4096, GQA 32q/8kv, head_dim 128, MLP 12288, vocab 512,
-bf16, random init) replaying 64 scripted TIM trajectories per GPU — the
-reference's own tool_chain_tree(32, seed=i) documents (tests/golden corpus) —
-with pruning buffer T=2.  Under torchrun each rank owns 64 requests
-(rank r: documents 64r..64r+63; 8 ranks = BASELINE config 3's 512 requests),
-weak scaling, no collective on the data path.
+bf16, random init) running 64 scripted TIM trajectories per GPU to completion
+-- the reference's own tool_chain_tree(32, seed=i) documents (tests/golden
+corpus) -- with pruning buffer T=2.  Under torchrun (or `--gpus N`, which
+re-executes itself under torchrun) the 64*N documents are dealt round-robin,
+document i to rank i % N (BASELINE config 3 at N=8), weak scaling, no
+collective on the data path.
 
 A "step" is one Engine.step() over the batch: host planning, K4/K5 device
 paging, and one batched forward of all requests' new tokens through every
-layer (decode rows + re-encode/tool rows).  The engine is fast-forwarded
-`--skip` steps to steady state first (untimed, full work), then W warm-up
-steps, then:
-  value : K steps replayed from device-resident step descriptors (host
-          planning done beforehand), CUDA events on the launching stream;
-  e2e   : the next K steps through the public Engine.step() API — host
-          planning, pinned H2D of each step descriptor, and a D2H read of the
-          step's greedy tokens every step.
+layer (decode rows + re-encode/tool rows).  The whole trajectory (~4.4K steps)
+runs; K steps sampled at a fixed stride over it (after W warm-up steps) are
+timed, so the timed steps carry the trajectory's own mix of decode-only and
+pruning / tool-response steps whatever K is:
+  value : the trajectory replayed from device-resident step descriptors (host
+          planning done beforehand); CUDA events bracket each timed step.
+  e2e   : a fresh engine runs every step through the public Engine.step();
+          each timed step is measured from the call to the D2H read of its
+          greedy tokens (host planning + pinned H2D of the step descriptor +
+          device work + D2H), synchronised on both sides.
 Tokens = tokens encoded for the first time (generated + tool tokens), the
 reference's output_len accounting (cli.py:130-134, scheduler.py:374-377).
+Both runs are checked against the REFERENCE Engine's per-step checksums of
+block tables, live lists and free list (tests/golden/bench_runs.*) and the
+device error word; a mismatch aborts the run.
 
 `--impl reference` times the reference's CPU implementation of the path (the
-numpy oracle restatement of model.py/scheduler.py — the Python reference
-itself cannot travel to the GPU box) on a bounded sample of the same
-workload, with every host thread BLAS can use.
+numpy oracle restatement of model.py -- the Python reference cannot travel to
+the GPU box) on the reference's own recorded per-step work of the same timed
+steps, with every host thread BLAS can use.
 """
 
 from __future__ import annotations
@@ -53,12 +59,6 @@ def peaks() -> dict:
         d = json.loads(p.read_text())
         return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured (MEASURED_PEAKS.json)"}
     return {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
-
-
-def workload_docs(rank: int, n: int):
-    from paper_2507_16784_b200.traces import load_corpus
-    docs = load_corpus(ROOT / "tests" / "golden" / "corpus_tool_chain32.json.gz")
-    return [docs[(rank * n + i) % len(docs)] for i in range(n)]
 
 
 class ClockSampler:
@@ -117,103 +117,159 @@ def reduce_over_ranks(dist, times, counts, device="cpu"):
 
 
 # --------------------------------------------------------------------- GPU arm
-def build_engine(rank: int, n_req: int, threshold: int, pool_per_req: int = 1600):
+def shard_docs(rank: int, world: int, per_gpu: int = PER_GPU) -> list[int]:
+    """BASELINE config 3: the 512 (= 64 x G) documents dealt round-robin,
+    document i to GPU i % G; G = 1 is config 2's 64."""
+    return [i for i in range(per_gpu * world) if i % world == rank]
+
+
+def build_engine(rank: int, n_req: int, threshold: int, pool_per_req: int = 1600, world: int = 1,
+                 model=None):
     import paper_2507_16784_b200 as tr
-    from paper_2507_16784_b200.traces import make_trace_from_text
+    from paper_2507_16784_b200.traces import load_corpus, make_trace_from_text
     cfg = tr.qwen3_8b_shape()
-    model = tr.B200Transformer(cfg)
-    traces = [make_trace_from_text(d) for d in workload_docs(rank, n_req)]
-    pool_pages = n_req * pool_per_req
+    model = model or tr.B200Transformer(cfg)
+    docs = load_corpus(ROOT / "tests" / "golden" / "corpus_tool_chain32.json.gz")
+    idx = shard_docs(rank, world, n_req)
     eng = tr.Engine(model, tr.BatchConfig(max_batch=n_req, buffer_threshold=threshold,
-                                          position_limit=cfg.position_limit, pool_pages=pool_pages,
+                                          position_limit=cfg.position_limit,
+                                          pool_pages=n_req * pool_per_req,
                                           max_queue=max(64, n_req), check_masks=False,
                                           max_output_tokens=20000))
-    for i, t in enumerate(traces):
-        eng.submit(f"q{rank}.{i}:", [tr.ToolSpec(n) for n in t.tool_names], script=t.script,
+    for i in idx:
+        t = make_trace_from_text(docs[i % len(docs)])
+        eng.submit(f"q{i}:", [tr.ToolSpec(n) for n in t.tool_names], script=t.script,
                    tool_responses=t.tool_responses)
     return eng, cfg, model
 
 
+def golden_rows(rank: int, world: int, threshold: int, n_req: int):
+    """The reference Engine's per-step checksums for this shard, when
+    tests/golden holds them (oracle/gen_golden.py gen_bench)."""
+    import gzip
+    import numpy as np
+    if threshold != 2 or n_req != PER_GPU:
+        return None
+    name = f"c2_g1_r0" if world == 1 else f"c3_g{world}_r{rank}"
+    meta_p = ROOT / "tests" / "golden" / "bench_runs.json.gz"
+    if not meta_p.exists():
+        return None
+    with gzip.open(meta_p, "rt") as f:
+        names = [s["name"] for s in json.load(f)["scenarios"]]
+    if name not in names:
+        return None
+    rows = np.load(ROOT / "tests" / "golden" / "bench_runs.npz")[name]
+    return name, {int(r[0]): [int(x) for x in r] for r in rows}
+
+
+def sampled_steps(n_steps: int, k: int, warmup: int) -> list[int]:
+    """K step indices at a fixed stride over the whole trajectory after the
+    W warm-up steps, so the timed steps carry the trajectory's own mix of
+    decode-only and mixed (prune re-encode / tool response) steps whatever K is."""
+    lo = min(warmup, n_steps - 1)
+    span = n_steps - lo
+    if k >= span:
+        return list(range(lo, n_steps))
+    return sorted({lo + (j * span) // k + (span // k) // 2 for j in range(k)})
+
+
 def run_gpu(args, rank: int, world: int, dist):
-    """value and e2e over the SAME K steps of the trajectories: engine A plans
-    them on the host and replays them from device-resident descriptors (value,
-    GPU-only); engine B — a fresh engine on the same traces, advanced to the
-    same step — runs them through the public Engine.step() (e2e: host planning,
-    pinned H2D of each step's descriptor, D2H of each step's greedy tokens)."""
+    """value and e2e over the SAME K steps of the trajectories (sampled at a
+    stride over the whole run, every step before and between them executed
+    untimed).  value: engine A plans the whole trajectory on the host, then
+    replays it from device-resident step descriptors; CUDA events bracket the
+    K sampled steps.  e2e: a fresh engine B on the same requests runs every
+    step through the public Engine.step(); each sampled step is timed from
+    the call to the D2H read of its greedy tokens (host planning, pinned H2D of
+    the step descriptor, device work, D2H), synchronised on both sides."""
     import torch
+    from paper_2507_16784_b200.checksum import device_hashes, host_hash, seq_hash_np
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-    cfg = None
+    gold = golden_rows(rank, world, args.threshold, args.batch)
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    def steps(eng, n):
-        tok = 0
-        for _ in range(n):
-            rep = eng.step()
-            tok += sum(rep.decoded.values())
-        return tok
-
-    def prepare():
-        eng, cfg_, model = build_engine(rank, args.batch, args.threshold)
-        t0 = time.perf_counter()
-        eng.runtime.precapture()
-        print(f"[rank {rank}] captured {len(eng.runtime.graphs)} step graphs in "
-              f"{time.perf_counter() - t0:.1f} s", file=sys.stderr)
-        steps(eng, args.skip)
-        steps(eng, args.warmup)
-        barrier()
-        return eng, cfg_, model
-
     # ---------------------------------------------------------------- value
-    eng, cfg, model = prepare()
+    eng, cfg, model = build_engine(rank, args.batch, args.threshold, world=world)
     rt = eng.runtime
-    kv_tok_layer = cfg.n_kv * cfg.head_dim * 2 * 2          # K+V bytes per token per layer (bf16)
-    q_o_bytes = cfg.heads * cfg.head_dim * 2 * 2            # q in + ctx out per decode query
-    attn_store = []
-    phase_store = [] if os.environ.get("TIMRUN_PHASES") else None
+    t0 = time.perf_counter()
+    rt.precapture()
+    print(f"[rank {rank}] captured {len(rt.graphs)} step graphs in {time.perf_counter() - t0:.1f} s",
+          file=sys.stderr)
     rt.recording = []
-    planned_tokens = steps(eng, args.steps)
+    step_tokens, step_free = [], []
+    while not eng.all_terminal():
+        rep = eng.step()
+        step_tokens.append(sum(rep.decoded.values()))
+        step_free.append(rep.pages_free)
     records, rt.recording = rt.recording, None
+    n_steps = len(step_tokens)
+    assert len(records) == n_steps, (len(records), n_steps)
+    # every rank times the same step indices of its own shard
+    if dist is not None:
+        t = torch.tensor([n_steps], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        n_steps_common = int(t.item())
+    else:
+        n_steps_common = n_steps
+    timed = sampled_steps(n_steps_common, args.steps, args.warmup)
+    timed_set = set(timed)
     resident = rt.replay_upload(records)
-    rows = sorted(sd.n_rows for sd, _, _ in records)
-    if os.environ.get("TIMRUN_STEPSTATS"):
-        for sd, _, _ in records:
-            if sd.ext:
-                segs = [sg[2] for sg in sd.segs if sg[2] > 1]
-                print(f"[step] rows={sd.n_rows} dec_tiles={len(sd.dec)} dec_keys={sum(d[2] for d in sd.dec)} "
-                      f"ext_items={len(sd.ext)} ext_blocks={sum((e[2] + 63) // 64 for e in sd.ext)} "
-                      f"split={sd.offsets.get('split_dec_ctas')}/{sd.offsets.get('split_ext_ctas')} "
-                      f"multi_segs={sorted(segs)[:12]}", file=sys.stderr)
+    checkpoints = {timed[len(timed) * q // 4] for q in (1, 2, 3)} if gold else set()
+    kv_tok_layer = cfg.n_kv * cfg.head_dim * 2 * 2          # K+V bytes per token per layer (bf16)
+    q_o_bytes = cfg.heads * cfg.head_dim * 2 * 2            # q in + ctx out per query row
+    attn_store, step_ev = [], []
     launches0 = rt.launches
-    rt.attn_events, rt.phase_events = attn_store, phase_store
+    launches_timed = 0
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
     clocks.start()
     barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    prof = os.environ.get("TIMRUN_PROFILE_TIMED") == "1"   # ncu --profile-from-start off: launch list of the value window
-    e0.record()
-    if prof:
-        torch.cuda.profiler.start()
-    rt.replay(resident)
-    if prof:
-        torch.cuda.profiler.stop()
-    e1.record()
+    for i, (sd, step, fw) in enumerate(resident):
+        if i in timed_set:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            rt.attn_events = attn_store
+            l0 = rt.launches
+            a.record()
+            rt._execute(sd, step, fw)
+            b.record()
+            rt.attn_events = None
+            launches_timed += rt.launches - l0
+            step_ev.append((a, b, i))
+        else:
+            rt._execute(sd, step, fw)
+        if i in checkpoints:
+            # step i+1 of the reference run: free stack vs the reference free list
+            torch.cuda.synchronize()
+            g = gold[1].get(i + 1)
+            sp = step_free[i]
+            ii = torch.arange(sp, dtype=torch.int64, device="cuda")
+            from paper_2507_16784_b200.checksum import weights_torch
+            fh = int(((eng.pool.free_stack[:sp].long() + 1) * weights_torch(ii)).sum()) if sp else 0
+            if g is not None and [sp, fh] != [g[5], g[10]]:
+                raise SystemExit(f"[rank {rank}] value run: free stack diverged from the reference at step {i + 1}")
     barrier()
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
+    rt.check()                                              # device error word of the whole run
+    ms = sum(a.elapsed_time(b) for a, b, _ in step_ev)
+    tokens = sum(step_tokens[i] for i in timed)
+    mixed_steps = sum(1 for i in timed if records[i][0].ext)
+    rows = sorted(records[i][0].n_rows for i in timed)
+    all_rows = [sd.n_rows for sd, _, _ in records]
+    mean_live = (sum(sum(sg[1] for sg in sd.segs) / max(len(sd.segs), 1) for sd, _, _ in records if sd.segs)
+                 / max(1, sum(1 for sd, _, _ in records if sd.segs)))
     # Fixed cost of bracketing ONE launch with CUDA events (an empty grid of the
     # attention kernel's shape, launched the same way): reported beside the
     # roofline so the per-launch figure can be read net of it.
     from paper_2507_16784_b200 import _lib as L
     floor = []
-    L.call("tim_noop", rt.sms, 288, 230000, torch.cuda.current_stream().cuda_stream)   # load the kernel
+    L.call("tim_noop", rt.sms, 288, 230000, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
-    torch.cuda._sleep(4_000_000)   # keep the GPU busy so the host enqueues ahead (no host gaps)
-    for i in range(60):
+    torch.cuda._sleep(4_000_000)
+    for _ in range(60):
         a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a_.record()
         L.call("tim_noop", rt.sms, 288, 230000, torch.cuda.current_stream().cuda_stream)
@@ -222,201 +278,217 @@ def run_gpu(args, rank: int, world: int, dist):
     torch.cuda.synchronize()
     floor_ms = sorted(a_.elapsed_time(b_) for a_, b_ in floor[10:])
     floor_ms = floor_ms[len(floor_ms) // 2]
-    launches = rt.launches - launches0
-    rt.attn_events = rt.phase_events = None
     weight_gb = model.weight_bytes() / 1e9
-    del eng, rt, model, resident, records
-    torch.cuda.empty_cache()
-
-    # ------------------------------------------------------------------ e2e
-    eng, _, model = prepare()
-    rt = eng.runtime
-    host_bufs = [torch.empty(args.batch * 2, dtype=torch.int32, pin_memory=True) for _ in range(2)]
-    result_sum = 0
-    host_step_ms = []
-    h2d = d2h = 0
-    e2e_tokens = 0
-    barrier()
-    w0 = time.perf_counter()
-    f0 = torch.cuda.Event(enable_timing=True)
-    f1 = torch.cuda.Event(enable_timing=True)
-    f0.record()
-    pend = None
-    for k in range(args.steps):
-        th = time.perf_counter()
-        rep = eng.step()
-        host_step_ms.append((time.perf_counter() - th) * 1000.0)
-        e2e_tokens += sum(rep.decoded.values())
-        h2d += rt._last_upload_bytes
-        toks = eng.last_step_tokens
-        if pend is not None:                       # read step k-1's result while step k runs
-            ev, buf, n = pend
-            ev.synchronize()
-            result_sum += int(buf[:n].sum())
-            pend = None
-        if toks is not None:
-            n = toks.numel()
-            buf = host_bufs[k % 2]
-            buf[:n].copy_(toks, non_blocking=True)   # D2H of the step's greedy tokens
-            ev = torch.cuda.Event()
-            ev.record()
-            pend = (ev, buf, n)
-            d2h += n * 4
-    if pend is not None:
-        pend[0].synchronize()
-        result_sum += int(pend[1][:pend[2]].sum())
-    f1.record()
-    barrier()
-    e2e_ms = f0.elapsed_time(f1)
-    wall_ms = (time.perf_counter() - w0) * 1000.0
-    assert e2e_tokens == planned_tokens, (e2e_tokens, planned_tokens)
-    hs = sorted(host_step_ms)
-    print(f"[rank {rank}] e2e host time inside Engine.step(): mean {sum(hs) / len(hs):.2f} ms, "
-          f"median {hs[len(hs) // 2]:.2f}, p90 {hs[int(len(hs) * 0.9)]:.2f}, max {hs[-1]:.2f}",
-          file=sys.stderr)
-    print(f"[rank {rank}] rows/step in the timed steps: min {rows[0]} median {rows[len(rows) // 2]} "
-          f"p90 {rows[int(len(rows) * 0.9)]} max {rows[-1]} mean {sum(rows) / len(rows):.0f}",
-          file=sys.stderr)
-    if phase_store:
-        import collections
-        agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0, 0])
-        for key, nd, kv, evs in phase_store:
-            a = agg[key]
-            a[0] += 1
-            a[1] += evs[0].elapsed_time(evs[1])
-            a[2] += evs[1].elapsed_time(evs[2])
-            a[3] += evs[2].elapsed_time(evs[3])
-            a[4] += kv
-        for key, (n, p0, p1, p2, kv) in sorted(agg.items()):
-            print(f"[phases] {key}: steps={n} pre={p0/n:.3f}ms attn0={p1/n:.3f}ms post={p2/n:.3f}ms "
-                  f"kv_tokens/step={kv/n:.0f}", file=sys.stderr)
-    # dominant-kernel roofline: the layer-0 attention launch of every value-block step
+    # dominant kernel: the layer-0 attention launch of every timed step
+    def attn_bytes(sd):
+        return sum(sg[1] + sg[2] for sg in sd.segs) * kv_tok_layer + sd.n_rows * q_o_bytes
     attn = [(a.elapsed_time(b), sd) for a, b, sd in attn_store]
-    attn_ms = sum(t for t, _ in attn) / max(len(attn), 1)
-    # unique K/V of every request's retained pages + its new rows, plus q in / ctx out per row
-    attn_bytes = sum(sum(sg[1] + sg[2] for sg in sd.segs) * kv_tok_layer + sd.n_rows * q_o_bytes
-                     for _, sd in attn) / max(len(attn), 1)
-    dec_only = [(t, sd) for t, sd in attn if sd.n_rows == len(sd.segs)]
-    mixed = [(t, sd) for t, sd in attn if sd.n_rows != len(sd.segs)]
-    mix_ms = sum(t for t, _ in mixed) / max(len(mixed), 1)
-    mix_bytes = sum(sum(sg[1] + sg[2] for sg in sd.segs) * kv_tok_layer + sd.n_rows * q_o_bytes
-                    for _, sd in mixed) / max(len(mixed), 1)
-    dec_ms = sum(t for t, _ in dec_only) / max(len(dec_only), 1)
-    dec_bytes = sum(sum(sg[1] + sg[2] for sg in sd.segs) * kv_tok_layer + sd.n_rows * q_o_bytes
-                    for _, sd in dec_only) / max(len(dec_only), 1)
-    mean_live = sum(sum(sg[1] for sg in sd.segs) / max(len(sd.segs), 1) for _, sd in attn) / max(len(attn), 1)
+    dec = [(t, sd) for t, sd in attn if not sd.ext]
+    mix = [(t, sd) for t, sd in attn if sd.ext]
 
-    print(f"[rank {rank}] value window: {planned_tokens} tokens in {ms:.1f} ms; e2e window: "
-          f"{e2e_tokens} tokens in {e2e_ms:.1f} ms GPU / {wall_ms:.1f} ms wall; "
-          f"launches={launches}", file=sys.stderr)
-    ms, e2e_ms, planned_tokens, e2e_tokens = reduce_over_ranks(
-        dist, [ms, e2e_ms], [planned_tokens, e2e_tokens], device="cuda")
-    return dict(ms=ms, e2e_ms=e2e_ms, wall_ms=wall_ms, tokens=planned_tokens, e2e_tokens=e2e_tokens,
-                attn_ms=attn_ms, attn_bytes=attn_bytes, launches=launches, clocks=clk,
-                dec_ms=dec_ms, dec_bytes=dec_bytes, n_dec_launches=len(dec_only), n_attn=len(attn),
-                mix_ms=mix_ms, mix_bytes=mix_bytes, n_mix_launches=len(mixed),
-                h2d=h2d / args.steps, d2h=d2h / args.steps, mean_live=mean_live,
-                weight_gb=weight_gb, floor_ms=floor_ms)
+    def agg(lst):
+        if not lst:
+            return {"achieved": None, "bytes_per_launch": 0.0, "ms_per_launch": 0.0, "launches": 0}
+        tm = sum(t for t, _ in lst) / len(lst)
+        by = sum(attn_bytes(sd) for _, sd in lst) / len(lst)
+        return {"achieved": by / (tm * 1e-3) / 1e9, "bytes_per_launch": by, "ms_per_launch": tm,
+                "launches": len(lst)}
+    del resident, records
+    # ------------------------------------------------------------------ e2e
+    eng2, _, _ = build_engine(rank, args.batch, args.threshold, world=world, model=model)
+    del eng, rt
+    torch.cuda.empty_cache()
+    rt2 = eng2.runtime
+    rt2.precapture()
+    host_buf = torch.empty(args.batch * 2, dtype=torch.int32, pin_memory=True)
+    e2e_s, e2e_tokens, h2d, d2h, result_sum = 0.0, 0, 0, 0, 0
+    host_ms = []
+    verified = []
+    barrier()
+    k = 0
+    while not eng2.all_terminal():
+        if k in timed_set:
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            th = time.perf_counter()
+            rep = eng2.step()
+            host_ms.append((time.perf_counter() - th) * 1e3)
+            toks = eng2.last_step_tokens
+            if toks is not None:
+                n = toks.numel()
+                host_buf[:n].copy_(toks)               # D2H of the step's greedy tokens (syncs)
+                result_sum += int(host_buf[:n].sum())
+                d2h += n * 4
+            torch.cuda.synchronize()
+            e2e_s += time.perf_counter() - w0
+            e2e_tokens += sum(rep.decoded.values())
+            h2d += rt2._last_upload_bytes
+        else:
+            rep = eng2.step()
+        k += 1
+        if gold and k in gold[1] and (k in {c + 1 for c in checkpoints} or eng2.all_terminal()):
+            pend = {rid: len(eng2.requests[rid].pending) for rid in rep.request_live}
+            mine = [rep.step, rep.active, rep.awaiting_tool, rep.finished, rep.failed, rep.pages_free,
+                    rep.flops_units, host_hash(rep.request_live, pend, rep.decoded), *device_hashes(eng2)]
+            if mine != gold[1][k]:
+                raise SystemExit(f"[rank {rank}] e2e run diverged from the reference ({gold[0]}) at step {k}")
+            verified.append(k)
+    barrier()
+    rt2.check()
+    assert e2e_tokens == tokens, (e2e_tokens, tokens)
+    hs = sorted(host_ms)
+    print(f"[rank {rank}] trajectory {n_steps} steps; timed {len(timed)} (stride "
+          f"{(n_steps_common - args.warmup) / max(len(timed), 1):.0f}); mixed steps timed {mixed_steps}; "
+          f"rows/step timed: min {rows[0]} median {rows[len(rows) // 2]} max {rows[-1]} mean "
+          f"{sum(rows) / len(rows):.0f} (whole run mean {sum(all_rows) / len(all_rows):.0f})",
+          file=sys.stderr)
+    print(f"[rank {rank}] e2e host time inside Engine.step(): mean {sum(hs) / len(hs):.2f} ms, "
+          f"median {hs[len(hs) // 2]:.2f}, max {hs[-1]:.2f}", file=sys.stderr)
+    print(f"[rank {rank}] reference checksums verified at steps {verified} ({gold[0] if gold else 'no golden'})",
+          file=sys.stderr)
+    print(f"[rank {rank}] value: {tokens} tokens in {ms:.1f} ms; e2e: {e2e_tokens} tokens in "
+          f"{e2e_s * 1e3:.1f} ms", file=sys.stderr)
+    ms_max, e2e_ms_max, tok_sum, e2e_tok_sum = reduce_over_ranks(
+        dist, [ms, e2e_s * 1e3], [tokens, e2e_tokens], device="cuda")
+    return dict(ms=ms_max, e2e_ms=e2e_ms_max, tokens=tok_sum, e2e_tokens=e2e_tok_sum,
+                n_timed=len(timed), n_steps=n_steps, mixed_timed=mixed_steps,
+                attn=agg(attn), dec=agg(dec), mix=agg(mix), launches=launches_timed, clocks=clk,
+                h2d=h2d / len(timed), d2h=d2h / len(timed), mean_live=mean_live,
+                weight_gb=weight_gb, floor_ms=floor_ms, verified=verified,
+                golden=gold[0] if gold else None, launches_total=rt2.launches)
 
 
 # --------------------------------------------------------------- CPU reference
-def cpu_reference(budget_s: float, steps: int, threshold: int, n_req: int = PER_GPU):
-    """Oracle (numpy) restatement of the reference per-request forward at the
-    C2 shape, timed on a bounded sample: for sampled (step, request) pairs the
-    request's actual work of that step (prefix m, n new tokens, taken from the
-    reference-exact accounting engine) through ONE layer, scaled by 36 layers
-    (+ logits).  Tokens/s = sampled tokens / sampled time (the reference runs
-    requests one after another, scheduler.py:304-316)."""
-    import numpy as np
-    from oracle import engine as oe
-    from oracle import model as om
-    from paper_2507_16784_b200.tokenizer import build_tokenizer
-    from paper_2507_16784_b200.traces import make_trace_from_text
-    from paper_2507_16784_b200.structure import StructureScanner
+def workload_config(world: int, args) -> dict:
+    """The `config` object of BOTH arms (identical, so the driver pairs them)."""
+    return {"workload": f"C2/C3: Qwen3-8B-shaped TIM decoder, {args.batch} tool_chain_tree(32) requests per GPU "
+                        f"(512 dealt round-robin at 8 GPUs), pruning buffer T={args.threshold}, run to completion",
+            "model": "qwen3-8b-shape: 36L, d4096, 32q/8kv x128, mlp 12288, vocab 512 (random init)",
+            "global_batch": args.batch * world, "seq_len": "retained working memory, mean ~640 tokens (max 1177)",
+            "parallelism": f"dp{world} (requests sharded, no collective)",
+            "window": f"{args.steps} engine steps at a fixed stride over the whole trajectory "
+                      f"(after {args.warmup} warm-up steps); every other step runs untimed",
+            "l2": "inputs larger than L2 (10.3 GB of weights + the retained KV read every step)"}
 
+
+def cpu_reference(budget_s: float, steps: int, warmup: int, threshold: int, n_req: int = PER_GPU):
+    """The reference's CPU algorithm for this path, timed on the host cores:
+    the numpy oracle of model.py:127-164 (+ GQA) at the Qwen3-8B shape, all
+    36 layers (one layer's weights shared by the 36, which leaves the work per
+    forward unchanged and keeps host memory at 0.7 GB), on the REFERENCE's own
+    per-step work: the (prefix m, n rows) of every forward the reference
+    Engine issued in the C2 run (tests/golden bench_runs.npz c2_work, recorded
+    by oracle/gen_golden.py).  The reference runs requests one after another
+    (scheduler.py:304-316), so a step costs the sum of its forwards.  Within
+    the budget, forwards are drawn uniformly at random from the same K timed
+    steps as the GPU arm; the steps' time is estimated as (#forwards) x (mean
+    sampled forward time) and tokens/s = the steps' first-encoded tokens over it.
+    Also reported: the scripted (page accounting only) oracle Engine's host
+    tokens/s on the same requests (SURVEY §8d leg 3)."""
+    import numpy as np
+    from oracle import model as om
+    from oracle.paging import PageTable
+
+    if threshold != 2 or n_req != PER_GPU:
+        raise SystemExit("the CPU reference leg is defined on the C2 workload (T=2, 64 requests)")
+    g = np.load(ROOT / "tests" / "golden" / "bench_runs.npz")
+    work, decoded = g["c2_work"], g["c2_decoded"]
+    n_steps = len(decoded)
+    timed = [i + 1 for i in sampled_steps(n_steps, steps, warmup)]       # reference step numbers
+    calls = work[np.isin(work[:, 0], timed)]
+    tokens = int(decoded[np.asarray(timed) - 1].sum())
+    cfg = om.Config(layers=36, heads=32, kv_heads=8, head_dim=128, mlp_dim=12288, vocab=512,
+                    position_limit=40960, rope_base=1e6)
+    rng = np.random.default_rng(0)
+    sc_ = np.float32(1.0 / np.sqrt(cfg.model_dim))
+    kvd = cfg.n_kv * cfg.head_dim
+
+    def mat(*shape):
+        return rng.standard_normal(shape, dtype=np.float32) * sc_
+    layer = {"wq": mat(4096, 4096), "wk": mat(4096, kvd), "wv": mat(4096, kvd), "wo": mat(4096, 4096),
+             "w1": mat(4096, 12288), "w2": mat(12288, 4096)}
+    w = {"emb": mat(512, 4096), "inv_freq": (1e6 ** (-np.arange(64) / 64)).astype(np.float32),
+         "layers": [layer] * 36}
+    model = om.Model(cfg, w)
+    max_pages = int((calls[:, 2] + calls[:, 3]).max()) + 1
+    pool = model.make_pool(max_pages)
+    pool.K[:] = rng.standard_normal(pool.K.shape, dtype=np.float32)
+    pool.V[:] = rng.standard_normal(pool.V.shape, dtype=np.float32)
+    order = rng.permutation(len(calls))
+    times = []
+    t_start = time.perf_counter()
+    for j in order:
+        _, _, m, n = (int(x) for x in calls[j])
+        pool.free_list = list(range(max_pages - 1, m - 1, -1))
+        pool.allocated = {p: "x" for p in range(m)}
+        t = PageTable("x")
+        t.pages = list(range(m))
+        toks = [int(x) for x in rng.integers(0, 512, n)]
+        c0 = time.perf_counter()
+        model.forward(toks, list(range(m, m + n)), t, pool)
+        times.append(time.perf_counter() - c0)
+        if time.perf_counter() - t_start > budget_s:
+            break
+    est_s = len(calls) * float(np.mean(times))
+    value = tokens / est_s
+    # leg 3: the scripted reference Engine (page accounting only) on the same requests
+    acc = scripted_engine_rate(min(budget_s / 3, 10.0), n_req, threshold)
+    import threadpoolctl
+    blas = threadpoolctl.threadpool_info()
+    threads = max([b.get("num_threads", 1) for b in blas] or [1])
+    return {"value": value, "unit": UNIT, "cores": int(threads), "kind": "port",
+            "sample": (f"{len(times)} of the {len(calls)} forwards the reference Engine issued in the "
+                       f"{len(timed)} timed steps of the C2 run (tool_chain_tree(32) x 64, T=2), each a "
+                       f"full 36-layer numpy forward (oracle/model.py = model.py:127-164 + GQA) at its "
+                       f"recorded (prefix m, rows n); {sum(times):.1f} s measured, steps' time estimated "
+                       f"as #forwards x mean = {est_s:.0f} s for {tokens} tokens; numpy {np.__version__}, "
+                       f"BLAS threads {threads}, os.cpu_count {os.cpu_count()}"),
+            "scripted_engine_tokens_per_s": acc}
+
+
+def scripted_engine_rate(budget_s: float, n_req: int, threshold: int) -> float:
+    """SURVEY §8d leg 3: the oracle's reference-order scripted Engine (page
+    accounting, no arithmetic) on the C2 requests: host tokens/s."""
+    from oracle import engine as oe
+    from paper_2507_16784_b200.structure import StructureScanner
+    from paper_2507_16784_b200.tokenizer import build_tokenizer
+    from paper_2507_16784_b200.traces import load_corpus, make_trace_from_text
     tok = build_tokenizer()
     P = 40960
     eng = oe.Engine(oe.Accounting(P), max_batch=n_req, threshold=threshold, position_limit=P,
                     pool_pages=n_req * 1600, max_queue=max(64, n_req), tokenize=tok.tokenize)
-    for i, d in enumerate(workload_docs(0, n_req)):
-        t = make_trace_from_text(d)
-        stream = []
-        sc = StructureScanner(tok)
-        evs = {}
-        call = 0
+    docs = load_corpus(ROOT / "tests" / "golden" / "corpus_tool_chain32.json.gz")
+    for i in shard_docs(0, 1, n_req):
+        t = make_trace_from_text(docs[i])
+        sc, evs, stream, call = StructureScanner(tok), [], [], 0
         for tid in t.script:
             for e in sc.feed(tid):
-                evs.setdefault(len(stream), []).append((e.kind, e.payload))
+                evs.append([e.kind, len(stream), e.depth, e.payload])
             stream.append(tid)
-            if evs.get(len(stream) - 1) and any(k == "ToolResultSlotOpened" for k, _ in evs[len(stream) - 1]):
-                for rt_ in tok.tokenize(json.dumps(t.tool_responses[call], separators=(",", ":"))):
+            if evs and evs[-1][0] == "ToolResultSlotOpened" and evs[-1][1] == len(stream) - 1:
+                text = json.dumps(t.tool_responses[call], separators=(",", ":"), ensure_ascii=False)
+                for rt_ in tok.tokenize(text):
                     for e in sc.feed(rt_):
-                        evs.setdefault(len(stream), []).append((e.kind, e.payload))
+                        evs.append([e.kind, len(stream), e.depth, e.payload])
                     stream.append(rt_)
                 call += 1
-        eng.submit(tok.tokenize(f"q0.{i}:"), t.script, t.tool_responses, evs)
-    # walk to steady state like the GPU arm, collecting per-request work
-    for _ in range(1500):
-        eng.step()
-    cfg = om.Config(layers=1, heads=32, kv_heads=8, head_dim=128, mlp_dim=12288, vocab=512,
-                    position_limit=P, rope_base=1e6)
-    rng = np.random.default_rng(0)
-    sc_ = 1.0 / np.sqrt(cfg.model_dim)
-    kvd = cfg.n_kv * cfg.head_dim
-    w = {"emb": (rng.standard_normal((512, 4096), dtype=np.float32) * sc_),
-         "inv_freq": (1e6 ** (-np.arange(64) / 64)).astype(np.float32),
-         "layers": [{"wq": rng.standard_normal((4096, 4096), dtype=np.float32) * sc_,
-                     "wk": rng.standard_normal((4096, kvd), dtype=np.float32) * sc_,
-                     "wv": rng.standard_normal((4096, kvd), dtype=np.float32) * sc_,
-                     "wo": rng.standard_normal((4096, 4096), dtype=np.float32) * sc_,
-                     "w1": rng.standard_normal((4096, 12288), dtype=np.float32) * sc_,
-                     "w2": rng.standard_normal((12288, 4096), dtype=np.float32) * sc_}]}
-    model = om.Model(cfg, w)
-    t_total = 0.0
-    tok_total = 0
-    samples = 0
-    t_start = time.perf_counter()
-    for s in range(max(steps, 1)):
-        before = {rid: (len(r.live), len(r.pending)) for rid, r in eng.requests.items()}
-        eng.step()
-        for rid, (m0, _) in before.items():
-            r = eng.requests[rid]
-            if r.status not in ("decoding", "awaiting_tool", "extending"):
-                continue
-            # work of this step: re-encode/new tokens at start len(live) after prune
-            n = len(r.live) - m0 if len(r.live) > m0 else 1
-            m = len(r.live) - n
-            if m < 0 or n <= 0:
-                continue
-            pool = model.make_pool(m + n + 1)
-            pool.K[: m] = rng.standard_normal((m, 1, 8, 128), dtype=np.float32)
-            pool.V[: m] = rng.standard_normal((m, 1, 8, 128), dtype=np.float32)
-            table = om.PagePool  # noqa: F841
-            from oracle.paging import PageTable
-            t = PageTable("x")
-            t.pages = list(range(m))
-            pool.free_list = [p for p in pool.free_list if p >= m]
-            for p in range(m):
-                pool.allocated[p] = "x"
-            toks = [int(x) for x in rng.integers(0, 512, n)]
-            c0 = time.perf_counter()
-            model.forward(toks, list(range(m, m + n)), t, pool)
-            dt = time.perf_counter() - c0
-            t_total += dt * 36            # 36 identical layers; logits (512x4096) are negligible
-            tok_total += 1 if n else 0
-            samples += 1
-            if time.perf_counter() - t_start > budget_s / max(steps, 1) * (s + 1):
-                break
-        if time.perf_counter() - t_start > budget_s:
-            break
-    value = tok_total / t_total if t_total else 0.0
-    threads = os.environ.get("OMP_NUM_THREADS") or str(os.cpu_count())
-    return {"value": value, "unit": UNIT, "cores": int(threads),
-            "kind": "port",
-            "sample": (f"{samples} sampled (step, request) decode forwards of the C2 workload "
-                       f"(tool_chain_tree(32), T=2, steady state after 1500 steps): numpy oracle "
-                       f"of model.py:127-164 for one layer x 36, sequential per request as "
-                       f"scheduler.py:304-316; {t_total:.1f} s of extrapolated CPU time")}
+        eng.submit(tok.tokenize(f"q{i}:"), t.script, t.tool_responses, oe.event_table(evs))
+    t0 = time.perf_counter()
+    toks = 0
+    while time.perf_counter() - t0 < budget_s and not eng.all_terminal():
+        toks += sum(eng.step()["decoded"].values())
+    return toks / (time.perf_counter() - t0)
+
+
+def respawn_under_torchrun(n: int) -> None:
+    """`python bench.py --gpus N` outside torchrun: re-exec as N ranks (one per GPU)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -424,7 +496,6 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--skip", type=int, default=1500)
     ap.add_argument("--batch", type=int, default=PER_GPU)
     ap.add_argument("--threshold", type=int, default=2)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -432,20 +503,20 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        respawn_under_torchrun(args.gpus)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    config = workload_config(world, args)
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = cpu_reference(args.cpu_budget, args.steps, args.threshold)
-        line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+        cb = cpu_reference(args.cpu_budget, args.steps, args.warmup, args.threshold, args.batch)
+        line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic", "impl": "reference",
-                "config": {"workload": "C2: Qwen3-8B-shaped TIM decoder, tool_chain_tree(32) x 64, T=2",
-                           "model": "qwen3-8b-shape (random init)", "global_batch": PER_GPU,
-                           "parallelism": "sequential CPU"},
-                "cpu_baseline": cb,
+                "data": "synthetic: reference tool_chain_tree(32) documents replayed as scripts; random-init weights",
+                "impl": "reference", "config": config, "cpu_baseline": cb,
                 "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
@@ -462,51 +533,40 @@ def main():
     res = run_gpu(args, rank, world, dist)
     if rank == 0:
         pk = peaks()
-        achieved = res["attn_bytes"] / (res["attn_ms"] * 1e-3) / 1e9 if res["attn_ms"] else 0.0
-        traffic = None
-        prof = ROOT / "profiles" / "decode_attention_traffic.json"
-        if prof.exists():
-            traffic = json.loads(prof.read_text()).get("bytes_per_launch")
+        a = res["attn"]
+        tr_path = ROOT / "profiles" / "attention_traffic.json"
+        traffic = json.loads(tr_path.read_text()) if tr_path.exists() else None
         cpu = None
         if world == 1 and args.cpu_budget > 0:
-            cpu = cpu_reference(args.cpu_budget, args.steps, args.threshold)
+            cpu = cpu_reference(args.cpu_budget, args.steps, args.warmup, args.threshold, args.batch)
         value = res["tokens"] / (res["ms"] * 1e-3)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": res["ms"] / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": res["ms"] / res["n_timed"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic: reference tool_chain_tree(32) documents replayed as scripts; random-init weights",
-            "config": {"workload": f"C2/C3: Qwen3-8B-shaped TIM decoder, {args.batch} tool_chain_tree(32) "
-                                   f"requests per GPU, pruning buffer T={args.threshold}",
-                       "model": "qwen3-8b-shape: 36L, d4096, 32q/8kv x128, mlp 12288, vocab 512",
-                       "global_batch": args.batch * world, "seq_len": f"retained mean {res['mean_live']:.0f}",
-                       "parallelism": f"dp{world} (requests sharded, no collective)",
-                       "skip_steps": args.skip,
-                       "l2": "inputs larger than L2 (weights %.1f GB + retained KV read every step)" % res["weight_gb"]},
-            "roofline": {"bound": "hbm", "kernel": "tim_attn_decode (layer 0 of each step)",
-                         "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+            "config": config,
+            "roofline": {"bound": "hbm", "kernel": "tim_attn_decode: decode tiles (K1) + tcgen05 items (K2), "
+                                                    "layer 0 of every timed step",
+                         "achieved": a["achieved"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": (a["achieved"] or 0.0) / pk["hbm_gbs"],
+                         "traffic": traffic["bytes_per_launch"] if traffic else None,
+                         "traffic_src": traffic["source"] if traffic else None,
                          "peak_src": pk["src"],
-                         "bytes_per_launch": res["attn_bytes"], "ms_per_launch": res["attn_ms"],
-                         "launches_timed": res["n_attn"],
+                         "bytes_per_launch": a["bytes_per_launch"], "ms_per_launch": a["ms_per_launch"],
+                         "launches_timed": a["launches"],
                          "event_floor_us": res["floor_ms"] * 1e3,
-                         "achieved_net_of_event_floor": res["attn_bytes"] / ((res["attn_ms"] - res["floor_ms"]) * 1e-3) / 1e9,
-                         "decode_only_steps": {"achieved": (res["dec_bytes"] / (res["dec_ms"] * 1e-3) / 1e9)
-                                               if res["dec_ms"] else None,
-                                               "bytes_per_launch": res["dec_bytes"],
-                                               "ms_per_launch": res["dec_ms"],
-                                               "launches": res["n_dec_launches"]},
-                         "mixed_steps": {"achieved": (res["mix_bytes"] / (res["mix_ms"] * 1e-3) / 1e9)
-                                         if res["mix_ms"] else None,
-                                         "bytes_per_launch": res["mix_bytes"],
-                                         "ms_per_launch": res["mix_ms"],
-                                         "launches": res["n_mix_launches"]}},
+                         "achieved_net_of_event_floor": a["bytes_per_launch"] / ((a["ms_per_launch"] - res["floor_ms"]) * 1e-3) / 1e9
+                         if a["launches"] else None,
+                         "decode_only_steps": res["dec"], "mixed_steps": res["mix"]},
             "cpu_baseline": cpu,
             "e2e": {"value": res["e2e_tokens"] / (res["e2e_ms"] * 1e-3), "unit": UNIT,
-                    "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
-                    "wall_ms_per_step": res["wall_ms"] / args.steps},
+                    "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"]},
             "gpu_launches": res["launches"],
             "clocks": res["clocks"],
+            "trajectory": {"steps": res["n_steps"], "timed_steps": res["n_timed"],
+                           "mixed_steps_timed": res["mixed_timed"], "mean_retained": res["mean_live"],
+                           "reference_checksums": res["golden"], "verified_at_steps": res["verified"]},
         }
         print(json.dumps(line))
     if dist is not None:

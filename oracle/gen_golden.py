@@ -322,18 +322,44 @@ BENCH_COLS = ["step", "active", "awaiting_tool", "finished", "failed", "pages_fr
               "host_hash", "table_hash", "live_hash", "free_hash"]
 
 
-def run_bench_scenario(name, docs, prompts, cfg, position_limit, every=1):
+class _WorkRecorder(ScriptedModel):
+    """ScriptedModel that logs every forward the reference Engine asks for:
+    (step, request index, start = prefix length m, n rows)."""
+
+    def __init__(self, position_limit):
+        super().__init__(position_limit=position_limit)
+        self.engine = None
+        self.calls = []
+
+    def _log(self, table, start, n):
+        self.calls.append((self.engine.step_index + 1, int(table.request_id[1:]), start, n))
+
+    def prefill(self, tokens, positions, table, pool):
+        self._log(table, len(table.pages), len(tokens))
+        return super().prefill(tokens, positions, table, pool)
+
+    def extend(self, tokens, start_position, table, pool):
+        self._log(table, start_position, len(tokens))
+        return super().extend(tokens, start_position, table, pool)
+
+
+def run_bench_scenario(name, docs, prompts, cfg, position_limit, every=1, record_work=False):
     """Reference scripted Engine over `docs`; one checksum row per `every` steps
     (and the last step).  Returns (rows int64 [n, 11], meta)."""
-    engine = Engine(ScriptedModel(position_limit=position_limit), cfg)
+    backend = _WorkRecorder(position_limit) if record_work else ScriptedModel(position_limit=position_limit)
+    engine = Engine(backend, cfg)
+    if record_work:
+        backend.engine = engine
     rids = []
     for doc, prompt in zip(docs, prompts):
         tr = make_trace_from_doc(doc)
         rids.append(engine.submit(prompt, [ToolSpec(n) for n in tr.tool_names], script=tr.script,
                                   tool_responses=tr.tool_responses or None))
     rows = []
+    decoded = []
     while not engine.all_terminal():
         rep = engine.step()
+        decoded.append(sum(rep.decoded.values()))
         if rep.step % every and not engine.all_terminal():
             continue
         pend = {rid: len(engine.requests[rid].pending) for rid in rep.request_live}
@@ -359,6 +385,9 @@ def run_bench_scenario(name, docs, prompts, cfg, position_limit, every=1):
             "applied_hash": _seq_hash([x for s in r.applied_spans for x in (s.start, s.end)]),
             "logical_hash": _seq_hash(r.logical),
         }
+    if record_work:
+        meta["work"] = np.asarray(backend.calls, dtype=np.int32)
+        meta["decoded"] = np.asarray(decoded, dtype=np.int32)
     return np.asarray(rows, dtype=np.int64), meta
 
 
@@ -381,7 +410,12 @@ def gen_bench():
         cfg = BatchConfig(max_batch=64, buffer_threshold=2, position_limit=40960, pool_pages=64 * 1600,
                           max_queue=64, check_masks=False, max_output_tokens=20000)
         t0 = time.time()
-        rows, meta = run_bench_scenario(name, [chain[i] for i in idx], [f"q{i}:" for i in idx], cfg, 40960)
+        rows, meta = run_bench_scenario(name, [chain[i] for i in idx], [f"q{i}:" for i in idx], cfg, 40960,
+                                        record_work=(G == 1))
+        if "work" in meta:
+            # every forward of the C2 run: the CPU baseline's per-step work list
+            arrays["c2_work"] = meta.pop("work")
+            arrays["c2_decoded"] = meta.pop("decoded")      # first-encoded tokens per step
         meta["docs"] = idx
         print(name, rows.shape, f"{time.time() - t0:.0f}s")
         arrays[name] = rows

@@ -32,17 +32,30 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Each translation unit compiles in its own nvcc process (in parallel,
+    relocatable device code off), then one host link produces the .so."""
     if not force and not _stale():
         return LIB
-    cmd = [
-        nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-        "--expt-relaxed-constexpr", *os.environ.get("TIMRUN_NVCC_FLAGS", "").split(), "-I", str(ROOT / "include"), "-I", str(CSRC),
-        "-o", str(LIB) + ".tmp", *[str(CSRC / s) for s in SOURCES], "-lcudart",
-    ]
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+             *os.environ.get("TIMRUN_NVCC_FLAGS", "").split(), "-I", str(ROOT / "include"), "-I", str(CSRC)]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        flags.insert(0, "-Xptxas=-v")
+
+    def compile_one(src: str) -> Path:
+        obj = objdir / (Path(src).stem + ".o")
+        cmd = [nvcc(), *flags, "-c", str(CSRC / src), "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    subprocess.run([nvcc(), *ARCH, "-shared", "-o", str(LIB) + ".tmp", *map(str, objs), "-lcudart"],
+                   check=True)
     os.replace(str(LIB) + ".tmp", LIB)
     return LIB
 

@@ -153,40 +153,44 @@ TIM_DEV int dec_grid(const tim_step_header& hd, int n_ctas) {
   return g0;
 }
 
-__global__ void attn_plan_kernel(const int32_t* __restrict__ step, const int32_t* __restrict__ tables,
-                                 int64_t tstride, int n_ctas, int max_dec, int d, float* __restrict__ ws) {
+// One warp per CTA record (8 per block): the tile search is the warp-parallel
+// seg_search (one round trip for <= 128 tiles) and the record's 32 page ids
+// are one load per lane, so the plan costs ~3 dependent round trips whatever
+// G is (the single-CTA serial version took 10.6 us per step).
+__global__ void __launch_bounds__(256) attn_plan_kernel(const int32_t* __restrict__ step,
+                                                        const int32_t* __restrict__ tables, int64_t tstride,
+                                                        int n_ctas, int max_dec, int d, float* __restrict__ ws) {
   const tim_step_header& hd = *reinterpret_cast<const tim_step_header*>(step);
   int32_t* plan = reinterpret_cast<int32_t*>(ws + ws_core_floats(n_ctas, max_dec, d));
   const int n_dec = hd.n_dec, N = hd.dec_total;
   const int want = (N + kMinTokensPerCta - 1) / kMinTokensPerCta;
   const int grid = dec_grid(hd, n_ctas);
   const int G = grid < want ? grid : want;
-  if (threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     plan[0] = hd.serial;
     plan[1] = G;
     plan[2] = N;
     plan[3] = 0;
   }
-  if (n_dec == 0 || N == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (n_dec == 0 || N == 0 || c >= G) return;
   const int32_t* dec = step + hd.off_dec;
   const int32_t* prefix = step + hd.off_dec_prefix;
-  for (int c = threadIdx.x; c < G; c += blockDim.x) {
-    const int start = (int)((int64_t)c * N / G), end = (int)((int64_t)(c + 1) * N / G);
-    int lo = 0, hi = n_dec - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (prefix[mid] <= start) lo = mid; else hi = mid - 1;
-    }
-    const int32_t* rec = dec + (int64_t)lo * TIM_DEC_FIELDS;
-    int32_t* o = plan + 8 + kPlanRec * c;
-    const int lo0 = prefix[lo], hi0 = prefix[lo + 1];
-    reinterpret_cast<int4*>(o)[0] = make_int4(start, end, lo, rec[1]);
-    reinterpret_cast<int4*>(o)[1] = make_int4(lo0, hi0, rec[4], rec[5]);
-    // the first page ids of the CTA's piece of that tile (padded with the last)
-    const int32_t* trow = tables + (int64_t)rec[1] * tstride;
-    const int p0 = start - lo0, n = (end < hi0 ? end : hi0) - lo0 - p0;
-    for (int k = 0; k < kPlanIds; ++k) o[8 + k] = trow[p0 + (k < n ? k : n - 1)];
+  const int start = (int)((int64_t)c * N / G), end = (int)((int64_t)(c + 1) * N / G);
+  const int lo = seg_search(prefix, n_dec, start, lane);
+  const int32_t* rec = dec + (int64_t)lo * TIM_DEC_FIELDS;
+  const int lo0 = __ldg(prefix + lo), hi0 = __ldg(prefix + lo + 1);
+  const int slot = __ldg(rec + 1), fresh = __ldg(rec + 4), hgrp = __ldg(rec + 5);
+  int32_t* o = plan + 8 + kPlanRec * c;
+  if (lane == 0) {
+    reinterpret_cast<int4*>(o)[0] = make_int4(start, end, lo, slot);
+    reinterpret_cast<int4*>(o)[1] = make_int4(lo0, hi0, fresh, hgrp);
   }
+  // the first page ids of the CTA's piece of that tile (padded with the last)
+  const int32_t* trow = tables + (int64_t)slot * tstride;
+  const int p0 = start - lo0, n = (end < hi0 ? end : hi0) - lo0 - p0;
+  for (int k = lane; k < kPlanIds; k += 32) o[8 + k] = __ldg(trow + p0 + (k < n ? k : n - 1));
 }
 
 // Body of K1 for CTA `cta` of the `grid` CTAs that stream the tile list.
@@ -949,8 +953,8 @@ extern "C" int64_t tim_decode_ws_floats(int32_t n_ctas, int32_t max_dec, int32_t
 extern "C" int32_t tim_attn_plan(const int32_t* step, const int32_t* block_tables, int64_t table_stride,
                                  int32_t n_ctas, int32_t max_dec, int32_t head_dim, float* ws, void* stream) {
   if (n_ctas <= 0 || n_ctas > kPlanMaxCtas) return TIM_OK;   // K1 falls back to its own search
-  attn_plan_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(step, block_tables, table_stride, n_ctas, max_dec,
-                                                        head_dim, ws);
+  attn_plan_kernel<<<(n_ctas + 7) / 8, 256, 0, (cudaStream_t)stream>>>(step, block_tables, table_stride,
+                                                                       n_ctas, max_dec, head_dim, ws);
   return check_launch("attn_plan");
 }
 

@@ -29,8 +29,12 @@ def _worker(rank, world, port, out):
     from paper_2507_16784_b200.structure import StructureScanner
     from paper_2507_16784_b200.tokenizer import build_tokenizer
     from paper_2507_16784_b200.traces import make_trace_from_text
+    from paper_2507_16784_b200.traces import load_corpus
     per = 4
-    docs = bench.workload_docs(rank, per)
+    corpus = load_corpus(bench.ROOT / "tests" / "golden" / "corpus_tool_chain32.json.gz")
+    idx = bench.shard_docs(rank, world, per)          # round-robin: document i -> rank i % world
+    assert idx == [i for i in range(per * world) if i % world == rank]
+    docs = [corpus[i] for i in idx]
     tok = build_tokenizer()
     eng = oe.Engine(oe.Accounting(4096), max_batch=per, threshold=2, position_limit=4096,
                     pool_pages=per * 1600, tokenize=tok.tokenize)
@@ -49,7 +53,7 @@ def _worker(rank, world, port, out):
                         evs.setdefault(len(stream), []).append((e.kind, e.payload))
                     stream.append(r)
                 call += 1
-        eng.submit(tok.tokenize(f"q{rank}.{i}:"), t.script, t.tool_responses, evs)
+        eng.submit(tok.tokenize(f"q{idx[i]}:"), t.script, t.tool_responses, evs)
     steps = tokens = 0
     while not eng.all_terminal():
         rep = eng.step()

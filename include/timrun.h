@@ -35,7 +35,8 @@ enum {
   TIM_SPAN_OUT_OF_RANGE = 4,  /* pruning.py:25-26  SpanOutOfRange (desync)       */
   TIM_BAD_ARGUMENT = 5,       /* ValueError                                      */
   TIM_CUDA_ERROR = 6,
-  TIM_UNSUPPORTED = 7
+  TIM_UNSUPPORTED = 7,
+  TIM_REJECTED = 8            /* tracker.py:56-65  Rejected (token not admitted) */
 };
 
 enum { TIM_DTYPE_F32 = 0, TIM_DTYPE_BF16 = 1 };
@@ -232,6 +233,67 @@ int32_t tim_gemm_trace(int32_t on, uint64_t* out, int32_t n);
 /* Greedy argmax over rows of logits [n, vocab] (lowest id on ties, model.py:186-192). */
 int32_t tim_argmax(const void* logits, int32_t n_rows, int32_t vocab, int32_t* out,
                    int32_t dtype, void* stream);
+
+/* Masked greedy pick (model.py:186-192, sample(logits, mask)): row r picks the
+ * highest logit among the ids set in mask row `mask_ids[r]` of the device mask
+ * table `masks` ([n_masks][words] uint32, bit t of word t/32 = id t admitted),
+ * lowest id on ties; mask_ids[r] < 0 = unmasked.  A row whose mask admits no
+ * id < vocab writes -1 (EmptyMask, model.py:189-190). */
+int32_t tim_masked_argmax(const void* logits, int32_t n_rows, int32_t vocab, const int32_t* mask_ids,
+                          const uint32_t* masks, int32_t words, int32_t* out, int32_t dtype, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Grammar tracker (host memory, no CUDA): replaces threadrun's Tracker
+ * (tracker.py:214-820) -- lifecycle events of the reasoning-tree document and
+ * the memoised admissible-next-token masks of allowed_mask (tracker.py:319-353).
+ * ------------------------------------------------------------------------- */
+typedef struct tim_grammar tim_grammar;
+typedef struct tim_tracker tim_tracker;
+
+/* Event kinds (tracker.py:33-40). */
+enum {
+  TIM_EV_TASK_OPENED = 0,
+  TIM_EV_THOUGHT_CLOSED = 1,
+  TIM_EV_TOOL_PARAMS_READY = 2,
+  TIM_EV_TOOL_RESULT_SLOT_OPENED = 3,
+  TIM_EV_SUBTASK_LIST_OPENED = 4,
+  TIM_EV_SUBTASK_LIST_CLOSED = 5,  /* a = span_start, b = span_end */
+  TIM_EV_TASK_CLOSED = 6,
+  TIM_EV_DONE = 7
+};
+
+/* ThreadGrammar(tools, depth_limit, tokenizer) (tracker.py:177-200): token
+ * pieces as concatenated bytes + n+1 offsets; tool names likewise.
+ * NULL on a bad argument. */
+tim_grammar* tim_grammar_create(const uint8_t* piece_bytes, const int32_t* piece_offsets, int32_t n_pieces,
+                                const uint8_t* tool_bytes, const int32_t* tool_offsets, int32_t n_tools,
+                                int32_t depth_limit);
+void tim_grammar_destroy(tim_grammar* g);
+/* Masks created so far (ids 0..count-1, creation order) and words per mask. */
+int32_t tim_grammar_mask_count(const tim_grammar* g);
+int32_t tim_grammar_mask_words(const tim_grammar* g);
+/* Copy out mask `mask_id` (host memory): admitted ids, the admitted ids that
+ * complete the document, and the admitted count.  Any pointer may be NULL. */
+int32_t tim_grammar_mask(const tim_grammar* g, int32_t mask_id, uint32_t* words, uint32_t* finish_words,
+                         int32_t* count);
+
+/* Tracker over one request's emission stream (grammar.tracker(), tracker.py:206-208). */
+tim_tracker* tim_tracker_create(tim_grammar* g);
+tim_tracker* tim_tracker_clone(const tim_tracker* t);
+void tim_tracker_destroy(tim_tracker* t);
+/* Tracker.feed (tracker.py:301-310): TIM_OK or TIM_REJECTED; *n_events events
+ * of this token, read with tim_tracker_event (fields = kind, offset, depth, a, b;
+ * name/params = the tool name and parameters text of tool events, valid until
+ * the next feed). */
+int32_t tim_tracker_feed(tim_tracker* t, int32_t token_id, int32_t* n_events);
+int32_t tim_tracker_feed_many(tim_tracker* t, const int32_t* ids, int32_t n, int32_t* at);
+int32_t tim_tracker_event(const tim_tracker* t, int32_t i, int32_t* fields, const char** name,
+                          int32_t* name_len, const char** params, int32_t* params_len);
+/* allowed_mask (tracker.py:319-335): memo id of the current state's mask. */
+int32_t tim_tracker_mask(tim_tracker* t, int32_t* mask_id, int32_t* count, int32_t* can_finish);
+int32_t tim_tracker_state(const tim_tracker* t, int32_t* consumed, int32_t* done, int32_t* depth,
+                          int32_t* reject_byte);
+const char* tim_tracker_context(const tim_tracker* t);
 
 #ifdef __cplusplus
 }

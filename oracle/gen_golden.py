@@ -440,6 +440,56 @@ def gen_bench():
     dump("bench_runs.json.gz", {"columns": BENCH_COLS, "scenarios": metas})
 
 
+def gen_masks():
+    """tracker.py allowed_mask at every position of documents, plus Rejected
+    messages: the C++ grammar tracker (csrc/grammar.cpp) must reproduce them.
+    Documents: 40 event-golden streams (depth limit 16, their tools) and
+    random mask walks (traces.random_mask_walk) under tools/no tools and depth
+    limits 16/2/1."""
+    import random
+    from threadrun.tracker import Rejected
+    from threadrun.traces import random_mask_walk
+    with gzip.open(OUT / "events.json.gz", "rt") as f:
+        ev = json.load(f)
+    docs = []
+    for r in ev[:40]:
+        docs.append({"tools": r["tool_names"], "depth": 16, "stream": r["stream"]})
+    for seed in range(60):
+        tools = [] if seed % 3 == 0 else ["search", "calc"]
+        depth = (16, 2, 1)[seed % 3 if seed % 5 else 0]
+        g = ThreadGrammar([ToolSpec(n) for n in tools], depth, TOK)
+        docs.append({"tools": tools, "depth": depth,
+                     "stream": random_mask_walk(g.tracker(), TOK, seed, budget=60 + 5 * seed)})
+    distinct: dict = {}
+    V = TOK.vocab_size
+    rng = random.Random(0)
+    for d in docs:
+        g = ThreadGrammar([ToolSpec(n) for n in d["tools"]], d["depth"], TOK)
+        tr = g.tracker()
+        idx, rejects = [], []
+        for pos, tid in enumerate(d["stream"] + [None]):
+            m = tr.allowed_mask()
+            bits = np.zeros(V, dtype=np.uint8)
+            bits[list(m.ids)] = 1
+            key = np.packbits(bits, bitorder="little").tobytes().hex()
+            idx.append(distinct.setdefault(key, len(distinct)))
+            if pos % 7 == 0:
+                # a few inadmissible tokens: the exception text (byte index + context)
+                bad = [t for t in range(V) if not m.admits(t)]
+                for t in rng.sample(bad, min(3, len(bad))):
+                    probe = tr.deep_copy()
+                    try:
+                        probe.feed(t)
+                        rejects.append([pos, t, None])
+                    except Rejected as e:
+                        rejects.append([pos, t, str(e)])
+            if tid is not None:
+                tr.feed(tid)
+        d["mask_idx"] = idx
+        d["rejects"] = rejects
+    dump("masks.json.gz", {"vocab": V, "masks": list(distinct), "docs": docs})
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["tokenizer", "events", "engine", "model", "corpus"]
     for w in which:

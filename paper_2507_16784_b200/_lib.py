@@ -21,6 +21,7 @@ TIM_SPAN_OUT_OF_RANGE = 4
 TIM_BAD_ARGUMENT = 5
 TIM_CUDA_ERROR = 6
 TIM_UNSUPPORTED = 7
+TIM_REJECTED = 8
 
 DTYPE_F32 = 0
 DTYPE_BF16 = 1
@@ -63,6 +64,22 @@ SIGNATURES = {
     "tim_gemm_ws_floats": (_i64, [_i32, _i32]),
     "tim_gemm_skinny": (_i32, [_p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _i32, _p]),
     "tim_gemm_trace": (_i32, [_i32, _p, _i32]),
+    "tim_masked_argmax": (_i32, [_p, _i32, _i32, _p, _p, _i32, _p, _i32, _p]),
+    # grammar tracker (host)
+    "tim_grammar_create": (_p, [_p, _p, _i32, _p, _p, _i32, _i32]),
+    "tim_grammar_destroy": (None, [_p]),
+    "tim_grammar_mask_count": (_i32, [_p]),
+    "tim_grammar_mask_words": (_i32, [_p]),
+    "tim_grammar_mask": (_i32, [_p, _i32, _p, _p, _p]),
+    "tim_tracker_create": (_p, [_p]),
+    "tim_tracker_clone": (_p, [_p]),
+    "tim_tracker_destroy": (None, [_p]),
+    "tim_tracker_feed": (_i32, [_p, _i32, _p]),
+    "tim_tracker_feed_many": (_i32, [_p, _p, _i32, _p]),
+    "tim_tracker_event": (_i32, [_p, _i32, _p, _p, _p, _p, _p]),
+    "tim_tracker_mask": (_i32, [_p, _p, _p, _p]),
+    "tim_tracker_state": (_i32, [_p, _p, _p, _p, _p]),
+    "tim_tracker_context": (_cp, [_p]),
 }
 
 

@@ -835,6 +835,28 @@ __global__ void attn_generic_kernel(const int32_t* __restrict__ step, const T* _
   }
 }
 
+// Split tiles are merged by a CTA that spins on the other pieces' counter
+// (K6).  That is deadlock-free only if every CTA of the grid can be resident at
+// once (the kernels never trigger their dependents early, so no later launch
+// can take the slots a waited-on CTA needs); refuse a grid larger than the
+// device's co-residency capacity for the kernel's threads and shared memory.
+template <class Kern>
+int32_t check_coresident(Kern kern, int threads, int smem, int n_ctas, int* cap, const char* name) {
+  if (*cap <= 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    *cap = per_sm * sms;
+  }
+  if (n_ctas > *cap) {
+    set_last_error("%s: grid of %d CTAs exceeds the %d co-resident CTAs the split-tile merge needs",
+                   name, n_ctas, *cap);
+    return TIM_BAD_ARGUMENT;
+  }
+  return TIM_OK;
+}
+
 template <int D, int HKV, int HG, int WPH>
 int32_t launch_tiles(const int32_t* step, int list, const void* q, void* out, const void* kl,
                      const void* vl, const int32_t* tables, int64_t tstride, int hq, float scale,
@@ -846,6 +868,8 @@ int32_t launch_tiles(const int32_t* step, int list, const void* q, void* out, co
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
+  static int cap = 0;
+  if (const int32_t rc = check_coresident(kern, C::THREADS, C::SMEM, n_ctas, &cap, "attn_tiles")) return rc;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
@@ -910,6 +934,9 @@ int32_t launch_step(const int32_t* step, const void* q, void* out, const void* k
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr = true;
   }
+  static int cap = 0;
+  if (const int32_t rc = check_coresident(kern, step_threads<D, HKV>(), SMEM, n_ctas, &cap, "attn_step"))
+    return rc;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[0].val.programmaticStreamSerializationAllowed = 1;

@@ -276,24 +276,32 @@ __global__ void silu_kernel(T* __restrict__ x, int64_t n) {
 }
 
 // One warp per row; ties resolve to the lowest id (np.argmax semantics).
+// With a mask table, only ids admitted by the row's mask compete
+// (np.where(allowed, logits, -inf), model.py:186-192); a row whose mask admits
+// nothing below `vocab` writes -1 (EmptyMask).
 template <typename T>
-__global__ void argmax_kernel(const T* __restrict__ logits, int n_rows, int vocab, int32_t* out) {
+__global__ void argmax_kernel(const T* __restrict__ logits, int n_rows, int vocab, int32_t* out,
+                              const int32_t* __restrict__ mask_ids, const uint32_t* __restrict__ masks,
+                              int words) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= n_rows) return;
   const T* row = logits + (int64_t)warp * vocab;
+  const int mid = mask_ids ? mask_ids[warp] : -1;
+  const uint32_t* mrow = mid >= 0 ? masks + (int64_t)mid * words : nullptr;
   float best = -INFINITY;
   int bi = 0x7fffffff;
   for (int i = lane; i < vocab; i += 32) {
+    if (mrow && (i >= 32 * words || !((mrow[i >> 5] >> (i & 31)) & 1u))) continue;
     const float v = to_f32(row[i]);
-    if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+    if (bi == 0x7fffffff || v > best || (v == best && i < bi)) { best = v; bi = i; }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float ov = __shfl_xor_sync(0xffffffffu, best, o);
     const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    if (oi != 0x7fffffff && (bi == 0x7fffffff || ov > best || (ov == best && oi < bi))) { best = ov; bi = oi; }
   }
-  if (lane == 0) out[warp] = bi == 0x7fffffff ? 0 : bi;
+  if (lane == 0) out[warp] = bi == 0x7fffffff ? (mrow ? -1 : 0) : bi;
 }
 
 }  // namespace tim
@@ -391,6 +399,17 @@ extern "C" int32_t tim_argmax(const void* logits, int32_t n_rows, int32_t vocab,
   if (n_rows <= 0) return TIM_OK;
   const int blocks = (n_rows * 32 + 255) / 256;
   TIM_DISPATCH(dtype, argmax_kernel<T><<<blocks, 256, 0, (cudaStream_t)stream>>>(
-                          (const T*)logits, n_rows, vocab, out));
+                          (const T*)logits, n_rows, vocab, out, nullptr, nullptr, 0));
   return check_launch("argmax");
+}
+
+extern "C" int32_t tim_masked_argmax(const void* logits, int32_t n_rows, int32_t vocab, const int32_t* mask_ids,
+                                     const uint32_t* masks, int32_t words, int32_t* out, int32_t dtype,
+                                     void* stream) {
+  if (n_rows <= 0) return TIM_OK;
+  if (!mask_ids || !masks || words <= 0) return TIM_BAD_ARGUMENT;
+  const int blocks = (n_rows * 32 + 255) / 256;
+  TIM_DISPATCH(dtype, argmax_kernel<T><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+                          (const T*)logits, n_rows, vocab, out, mask_ids, masks, words));
+  return check_launch("masked_argmax");
 }

@@ -64,6 +64,10 @@ class DevicePagePool:
         self._codes: dict[object, int] = {}
         self._owners: list[object] = []
         self._scratch = None
+        # host mirror of `owner` for the per-call API (DoubleFree checks without
+        # a device readback); invalidated by the engine's planned ops
+        self._owner_host = np.full(capacity, -1, dtype=np.int32)
+        self._mirror_valid = True
         self.K_layers = self.V_layers = None
         if kv_shape is not None:
             layers, heads, head_dim = kv_shape
@@ -132,7 +136,9 @@ class DevicePagePool:
         sd.op(L.OP_FREE, slot, table_off, n, self._sp, owner_code)
         self._sp += n
 
-    def run_ops(self, step_dev: torch.Tensor, tables: torch.Tensor) -> None:
+    def run_ops(self, step_dev: torch.Tensor, tables: torch.Tensor, _percall: bool = False) -> None:
+        if not _percall:
+            self._mirror_valid = False
         L.call("tim_page_ops", step_dev.data_ptr(), self.free_stack.data_ptr(),
                self.owner.data_ptr(), self.capacity, tables.data_ptr(), tables.shape[1],
                self.err.data_ptr(), stream_handle())
@@ -147,9 +153,27 @@ class DevicePagePool:
 
     # ---------------------------------------------- per-call API (paging.py:52-67)
     def _scratch_row(self, n: int) -> torch.Tensor:
-        if self._scratch is None or self._scratch.shape[1] < n:
-            self._scratch = torch.empty((1, max(n, 64)), dtype=torch.int32, device=self.device)
+        """(1, >= n + 2) int32: n page ids, then a copy of the error word, so one
+        D2H read returns both."""
+        if self._scratch is None or self._scratch.shape[1] < n + 2:
+            self._scratch = torch.empty((1, max(n + 2, 64)), dtype=torch.int32, device=self.device)
         return self._scratch
+
+    def _owners_host(self) -> np.ndarray:
+        if not self._mirror_valid:
+            self._owner_host = self.owner.cpu().numpy().copy()
+            self._mirror_valid = True
+        return self._owner_host
+
+    def _run_percall(self, sd: StepDesc, scratch: torch.Tensor, n: int) -> np.ndarray:
+        step = torch.from_numpy(sd.pack()).pin_memory().to(self.device, non_blocking=True)
+        self.run_ops(step, scratch, _percall=True)
+        scratch[0, n:n + 2].copy_(self.err)
+        host = scratch[0, : n + 2].cpu().numpy()  # the one synchronisation of the call
+        if host[n] != L.TIM_OK:
+            self.err.zero_()
+            raise_device_error(int(host[n]), int(host[n + 1]))
+        return host[:n]
 
     def alloc(self, request_id, n: int) -> list[int]:
         if n < 0:
@@ -158,20 +182,19 @@ class DevicePagePool:
             raise OutOfPages(n, self._sp)
         if n == 0:
             return []
-        scratch = self._scratch_row(n)
+        code = self.owner_code(request_id)
         sd = StepDesc()
-        self.plan_alloc(sd, 0, 0, n, self.owner_code(request_id))
-        step = torch.from_numpy(sd.pack()).to(self.device)
-        self.run_ops(step, scratch)
-        ids = scratch[0, :n].cpu().tolist()
-        self.check()
-        return ids
+        self.plan_alloc(sd, 0, 0, n, code)
+        ids = self._run_percall(sd, self._scratch_row(n), n)
+        if self._mirror_valid:
+            self._owner_host[ids] = code
+        return ids.tolist()
 
     def free(self, page_ids) -> None:
         ids = [int(p) for p in page_ids]
         if not ids:
             return
-        own = self.owner.cpu().numpy()
+        own = self._owners_host()
         bad = None
         good = []
         seen = set()
@@ -183,12 +206,12 @@ class DevicePagePool:
             good.append(pid)
         if good:
             scratch = self._scratch_row(len(good))
-            scratch[0, : len(good)] = torch.tensor(good, dtype=torch.int32, device=self.device)
+            scratch[0, : len(good)].copy_(torch.tensor(good, dtype=torch.int32).pin_memory(),
+                                          non_blocking=True)
             sd = StepDesc()
             self.plan_free(sd, 0, 0, len(good), ANY_OWNER)
-            step = torch.from_numpy(sd.pack()).to(self.device)
-            self.run_ops(step, scratch)
-            self.check()
+            self._run_percall(sd, scratch, len(good))
+            own[good] = -1
         if bad is not None:
             raise DoubleFree(bad)
 

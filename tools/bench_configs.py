@@ -82,9 +82,11 @@ def run_c5(a):
 
 
 def run_c4(a):
+    """C4 long horizon.  --complete runs every request to the end of its
+    trajectory (134,480 generated tokens each) and times every step."""
     cfg = tr.qwen3_8b_shape(position_limit=16384)
     model = tr.B200Transformer(cfg)
-    n = 32
+    n = a.requests
     eng = tr.Engine(model, tr.BatchConfig(max_batch=n, buffer_threshold=2, position_limit=16384,
                                           pool_pages=n * (a.prompt + 2048), max_queue=64, check_masks=False,
                                           max_output_tokens=140_000))
@@ -96,43 +98,94 @@ def run_c4(a):
         eng.submit(prompt + f"g{i}:", script=t.script)
     eng.runtime.precapture()
     t0 = time.perf_counter()
-    for _ in range(a.skip):
-        eng.step()
-    w = timed_window(eng, a.steps)
+    if a.complete:
+        w = dict(ms=0.0, tokens=0, pages_freed=0, prune_jobs=0, kv_tokens=0, prologue_ms=0.0)
+        steps = 0
+        while not eng.all_terminal():
+            wi = timed_window(eng, 256)
+            for k in w:
+                w[k] += wi[k]
+            steps += 256
+            if steps % 16384 == 0:
+                eng.runtime.check()
+        eng.runtime.check()
+        steps = eng.step_index
+    else:
+        for _ in range(a.skip):
+            eng.step()
+        w = timed_window(eng, a.steps)
+        steps = a.steps
     reqs = list(eng.requests.values())
-    return {"config": "C4 long horizon: 32 x deep_recursion(8 levels, 3-way, 16-char texts) "
-                      f"= 134,480 generated tokens each, {a.prompt}-token prompt, T=2, position limit 16384",
-            "skip_steps": a.skip, "steps": a.steps, "tokens_per_s": w["tokens"] / (w["ms"] * 1e-3),
-            "ms_per_step": w["ms"] / a.steps,
-            "pages_freed_per_s": w["pages_freed"] / (w["ms"] * 1e-3),
-            "prune_jobs_per_step": w["prune_jobs"] / a.steps,
-            "k4_k5_staging_us_per_step": 1000 * w["prologue_ms"] / a.steps,
-            "mean_retained_per_request": w["kv_tokens"] / a.steps / n,
-            "max_cache_so_far": max(r.metrics.max_cache for r in reqs),
-            "pruned_tokens_so_far": sum(r.metrics.pruned_tokens for r in reqs),
-            "host_s_skip": time.perf_counter() - t0}
+    out = {"config": f"C4 long horizon: {n} x deep_recursion(8 levels, 3-way, 16-char texts) "
+                     f"= 134,480 generated tokens each, {a.prompt}-token prompt, T=2, position limit 16384",
+           "requests": n, "steps": steps, "tokens_per_s": w["tokens"] / (w["ms"] * 1e-3),
+           "ms_per_step": w["ms"] / steps,
+           "pages_freed_per_s": w["pages_freed"] / (w["ms"] * 1e-3),
+           "pages_freed": w["pages_freed"],
+           "prune_jobs_per_step": w["prune_jobs"] / steps,
+           "k4_k5_staging_us_per_step": 1000 * w["prologue_ms"] / steps,
+           "mean_retained_per_request": w["kv_tokens"] / steps / n,
+           "max_cache": max(r.metrics.max_cache for r in reqs),
+           "pruned_tokens": sum(r.metrics.pruned_tokens for r in reqs),
+           "host_s": time.perf_counter() - t0}
+    if a.complete:
+        out.update(
+            output_len=[r.metrics.output_len for r in reqs],
+            statuses=[r.status.value for r in reqs],
+            leaked_pages=eng.pool.capacity - eng.pool.free_count,
+            kv_pruned_pct=[eng.result(r.rid)["metrics"].get("kv_pruned_pct") for r in reqs])
+        assert out["leaked_pages"] == 0 and all(x == 134480 for x in out["output_len"]), out
+        assert out["max_cache"] < 16384
+    else:
+        out["skip_steps"] = a.skip
+    return out
 
 
 def run_c1(a):
-    from paper_2507_16784_b200.traces import deep_recursion_doc as _d  # noqa: F401
+    """C1 tiny fp32, batch 1, deep(3,2), T=1: the B200 engine (graphs captured
+    before timing) beside the REFERENCE Engine + TinyTransformer (baseline/_ref,
+    numpy, this host's cores) on the same trace -- SURVEY §8d CPU leg 1."""
     doc = deep_recursion_doc(3, 2, seed=0)
     t = make_trace_from_text(doc)
-    cfg = tr.ModelConfig(layers=2, heads=4, head_dim=32, vocab=512, position_limit=2048)
-    eng = tr.Engine(tr.B200Transformer(cfg), tr.BatchConfig(buffer_threshold=1, position_limit=2048,
-                                                            pool_pages=4096))
-    eng.submit("p:", script=t.script)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    steps = 0
-    while not eng.all_terminal():
-        eng.step()
-        steps += 1
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    res = next(iter(eng.results.values()))
-    return {"config": "C1 tiny fp32 (2 layers, 4 heads, d_model 128), batch 1, deep(3,2), T=1",
-            "steps": steps, "wall_s": dt, "tokens_per_s": res["metrics"]["output_len"] / dt,
-            "metrics": res["metrics"]}
+
+    def ours():
+        cfg = tr.ModelConfig(layers=2, heads=4, head_dim=32, vocab=512, position_limit=2048)
+        eng = tr.Engine(tr.B200Transformer(cfg), tr.BatchConfig(buffer_threshold=1, position_limit=2048,
+                                                                pool_pages=4096))
+        eng.runtime.precapture()
+        eng.submit("p:", script=t.script)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        while not eng.all_terminal():
+            eng.step()
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0, next(iter(eng.results.values()))
+
+    ours()                              # warm (allocator, cuBLAS handles)
+    dt, res = ours()
+    out = {"config": "C1 tiny fp32 (2 layers, 4 heads, d_model 128), batch 1, deep(3,2), T=1",
+           "wall_s": dt, "tokens_per_s": res["metrics"]["output_len"] / dt, "metrics": res["metrics"]}
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "threadrun").is_dir():
+        sys.path.insert(0, str(ref))
+        from threadrun import model as rm, scheduler as rs
+        import os as _os
+        best = None
+        for _ in range(3):
+            eng = rs.Engine(rm.TinyTransformer(rm.ModelConfig(layers=2, heads=4, head_dim=32, vocab=512,
+                                                              position_limit=2048)),
+                            rs.BatchConfig(buffer_threshold=1, position_limit=2048, pool_pages=4096))
+            rid = eng.submit("p:", script=t.script)
+            t0 = time.perf_counter()
+            eng.run_until_done()
+            d = time.perf_counter() - t0
+            best = d if best is None else min(best, d)
+            rres = eng.result(rid)
+        assert rres["text"] == res["text"] and rres["metrics"] == res["metrics"]
+        out["reference"] = {"impl": "threadrun Engine + TinyTransformer (baseline/_ref, unmodified)",
+                            "wall_s": best, "tokens_per_s": rres["metrics"]["output_len"] / best,
+                            "cores": _os.cpu_count(), "kind": "reference"}
+    return out
 
 
 if __name__ == "__main__":
@@ -141,5 +194,7 @@ if __name__ == "__main__":
     ap.add_argument("--skip", type=int, default=600)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--prompt", type=int, default=12000, help="C4 prompt tokens")
+    ap.add_argument("--requests", type=int, default=32, help="C4 requests")
+    ap.add_argument("--complete", action="store_true", help="C4: run every request to completion")
     a = ap.parse_args()
     print(json.dumps({"c1": run_c1, "c4": run_c4, "c5": run_c5}[a.config](a)))

@@ -460,7 +460,7 @@ def scripted_engine_rate(budget_s: float, n_req: int, threshold: int) -> float:
     """SURVEY §8d leg 3: the oracle's reference-order scripted Engine (page
     accounting, no arithmetic) on the C2 requests: host tokens/s."""
     from oracle import engine as oe
-    from paper_2507_16784_b200.structure import StructureScanner
+    from paper_2507_16784_b200.grammar import Grammar
     from paper_2507_16784_b200.tokenizer import build_tokenizer
     from paper_2507_16784_b200.traces import load_corpus, make_trace_from_text
     tok = build_tokenizer()
@@ -470,7 +470,7 @@ def scripted_engine_rate(budget_s: float, n_req: int, threshold: int) -> float:
     docs = load_corpus(ROOT / "tests" / "golden" / "corpus_tool_chain32.json.gz")
     for i in shard_docs(0, 1, n_req):
         t = make_trace_from_text(docs[i])
-        sc, evs, stream, call = StructureScanner(tok), [], [], 0
+        sc, evs, stream, call = Grammar(t.tool_names, 16, tok).tracker(), [], [], 0
         for tid in t.script:
             for e in sc.feed(tid):
                 evs.append([e.kind, len(stream), e.depth, e.payload])

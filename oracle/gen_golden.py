@@ -490,6 +490,39 @@ def gen_masks():
     dump("masks.json.gz", {"vocab": V, "masks": list(distinct), "docs": docs})
 
 
+def gen_unscripted():
+    """Unscripted (grammar-masked greedy) runs of the reference Engine +
+    TinyTransformer (fp32, reference weights): per step the report, every
+    request's page-table / live-list CRC and the free-list CRC; per request the
+    token stream, status and result.  Requests hit their max_output_tokens at
+    different steps, so each TokenLimit failure frees pages between two other
+    requests' allocations (scheduler.py:304-316, 536-548)."""
+    scens = []
+    for seed, prompts, tools, limits, T in [
+            (3, ["task:", "q:", "x"], [[], ["search"], []], [60, 200, 130], 1),
+            (0, ["task:"], [[]], [150], 0),
+            (1, ["a:", "b:", "c:", "d:"], [[], [], ["calc", "search"], []], [45, 90, 120, 75], 2)]:
+        m = TinyTransformer(ModelConfig(layers=2, heads=4, head_dim=32, vocab=512, position_limit=512,
+                                        seed=seed))
+        e = Engine(m, BatchConfig(max_batch=len(prompts), buffer_threshold=T, position_limit=512,
+                                  pool_pages=2048, max_output_tokens=400))
+        rids = [e.submit(p, [ToolSpec(n) for n in tl], max_output_tokens=lim)
+                for p, tl, lim in zip(prompts, tools, limits)]
+        steps = []
+        while not e.all_terminal():
+            rep = e.step()
+            steps.append([rep.step, rep.active, rep.finished, rep.failed, rep.pages_free, rep.flops_units,
+                          [crc(e.requests[r].table.pages) for r in rids],
+                          [crc(e.requests[r].live) for r in rids], crc(e.pool.free_list)])
+        scens.append({"seed": seed, "prompts": prompts, "tools": tools, "limits": limits, "threshold": T,
+                      "rids": rids, "steps": steps,
+                      "requests": {r: {"logical": e.requests[r].logical, "status": e.requests[r].status.value,
+                                       "result": e.result(r), "evictions": [[s.start, s.end] for s in
+                                                                            e.requests[r].eviction_log]}
+                                   for r in rids}})
+    dump("unscripted_runs.json.gz", scens)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["tokenizer", "events", "engine", "model", "corpus"]
     for w in which:

@@ -12,7 +12,8 @@ __version__ = "0.1.0"
 
 from .tokenizer import ByteTokenizer, build_tokenizer
 from .spans import TokenSpan
-from .structure import Rejected, StructureEvent, StructureScanner
+from .grammar import Grammar, TokenMask, Tracker
+from .structure import Rejected, StructureEvent
 from .paging import DevicePagePool, DoubleFree, KvPage, OutOfPages, PagePool, PageTable, gather
 from .pruning import (PruneBuffer, PrunePlan, RequestMetrics, SpanOutOfRange, ZeroLength, apply,
                       coalesce, kv_pruned_pct, oracle_evictions)
@@ -25,7 +26,7 @@ from .traces import Trace, make_trace_from_text
 
 __all__ = [
     "ByteTokenizer", "build_tokenizer", "TokenSpan", "Rejected", "StructureEvent",
-    "StructureScanner", "DevicePagePool", "DoubleFree", "KvPage", "OutOfPages", "PagePool",
+    "Grammar", "TokenMask", "Tracker", "DevicePagePool", "DoubleFree", "KvPage", "OutOfPages", "PagePool",
     "PageTable", "gather", "PruneBuffer", "PrunePlan", "RequestMetrics", "SpanOutOfRange",
     "ZeroLength", "apply", "coalesce", "kv_pruned_pct", "oracle_evictions", "B200Transformer",
     "EmptyExtend", "EmptyMask", "ModelConfig", "PositionOverflow", "ScriptedModel",

@@ -424,8 +424,11 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
         mbar_arrive(&p_ready[b]);
         if (threadIdx.x == 0) TCT(5, gb);
       }
-      // epilogue: O / l of this row -> bf16 -> out
+      // epilogue: O / l of this row -> bf16 -> out.  Observe the last two PV
+      // phases (one per pv_done barrier): every phase of the ring is waited on
+      // by someone (the loop above waited the phases of blocks j-2).
       const int gl = gb - 1;
+      if (nblk >= 2) mbar_wait(&pv_done[(gl - 1) & 1], ((gl - 1) >> 1) & 1);
       mbar_wait(&pv_done[gl & 1], (gl >> 1) & 1);
       fence_after();
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;

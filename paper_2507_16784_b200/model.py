@@ -173,6 +173,24 @@ class StepRuntime:
         self.prologue_events = None  # list -> CUDA events around K4 + K5 + staging
         self.phase_events = None     # list -> CUDA events around pre / attn0 / post (diagnostics)
         self.attn_events = None      # list -> CUDA events around layer-0 decode attention
+        # admissible-token masks of unscripted picks (grammar.py), by device id;
+        # a fixed buffer, so captured graphs keep their address
+        self.mask_words = (getattr(model, "vocab_size", 512) + 31) // 32 if model is not None else 16
+        self.masks = torch.zeros((self.MASK_CAP, self.mask_words), dtype=torch.int32, device=self.dev)
+        self.n_masks = 0
+
+    MASK_CAP = 1 << 14
+
+    def add_mask(self, words: np.ndarray) -> int:
+        """Store one admissible-token bitmask on the device; returns its id."""
+        if self.n_masks >= self.MASK_CAP:
+            raise RuntimeError("device mask table full (raise StepRuntime.MASK_CAP)")
+        row = np.zeros(self.mask_words, dtype=np.uint32)
+        n = min(len(words), self.mask_words)
+        row[:n] = words[:n]
+        self.masks[self.n_masks].copy_(torch.from_numpy(row.view(np.int32)))
+        self.n_masks += 1
+        return self.n_masks - 1
 
     # ----------------------------------------------------------- buffers
     def grow_logical(self, n: int) -> None:
@@ -624,7 +642,8 @@ class B200Transformer:
         n += self._gemm(rt, li, 3, rt.u, rt.h, rt.h, T)
         return 1 + n
 
-    def _post(self, rt, sp: int, step: torch.Tensor, T: int, n_last: int, has_ext: bool):
+    def _post(self, rt, sp: int, step: torch.Tensor, T: int, n_last: int, has_ext: bool,
+              mask_off: int | None = None):
         cfg, st, td = self.config, stream_handle(), self.config.tim_dtype
         dm = cfg.model_dim
         n = self._layer_tail(rt, 0, T)
@@ -639,7 +658,10 @@ class B200Transformer:
         L.call("tim_rmsnorm", hl.data_ptr(), dm, xl.data_ptr(), dm, n_last, dm, 1e-6, td, st)
         logits = torch.matmul(xl, self.emb_t).float()
         toks = torch.empty(n_last, dtype=torch.int32, device=self.dev)
-        L.call("tim_argmax", logits.data_ptr(), n_last, cfg.vocab, toks.data_ptr(), L.DTYPE_F32, st)
+        # masked greedy pick (model.py:186-192): mask ids follow `last` in the descriptor
+        mask_ids = step.data_ptr() + (off + n_last if mask_off is None else mask_off) * 4
+        L.call("tim_masked_argmax", logits.data_ptr(), n_last, cfg.vocab, mask_ids, rt.masks.data_ptr(),
+               rt.mask_words, toks.data_ptr(), L.DTYPE_F32, st)
         return n + 2, logits, toks
 
     def forward_rows(self, rt: StepRuntime, step: torch.Tensor, sd: StepDesc):
@@ -678,7 +700,8 @@ class B200Transformer:
             sp = step.data_ptr()
             n = self._pre(rt, sp, T)
             n += self._attn(rt, sp, 0, T, has_ext, ev)
-            m, logits, toks = self._post(rt, sp, step, T, len(sd.last), has_ext)
+            m, logits, toks = self._post(rt, sp, step, T, len(sd.last), has_ext,
+                                         sd.offsets["off_last_mask"])
             rt.launches += n + m
         if ev:
             timed.append((ev[0][0], ev[0][1], sd))

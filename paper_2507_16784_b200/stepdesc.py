@@ -24,7 +24,7 @@ class StepDesc:
     """Accumulates one step's records and packs them into an int32 array."""
 
     __slots__ = ("new", "segs", "dec", "ext", "jobs", "spans", "ops", "phase_starts", "last",
-                 "n_rows", "_last_kind", "offsets", "rows_pad", "last_pad", "ctas", "serial")
+                 "n_rows", "_last_kind", "offsets", "rows_pad", "last_pad", "ctas", "serial", "last_mask")
 
     def __init__(self):
         self.new: list = []      # (slot, logical_idx, token, row, live_idx)
@@ -36,6 +36,7 @@ class StepDesc:
         self.ops: list = []      # (kind, slot, table_off, count, sp_before, owner)
         self.phase_starts: list = []
         self.last: list = []     # rows whose logits are produced
+        self.last_mask: list = []  # per `last` row: device mask id of its masked pick (-1: none)
         self.n_rows = 0
         self._last_kind = -1
         self.offsets: dict = {}
@@ -153,6 +154,8 @@ class StepDesc:
 
         last = list(self.last) + [0] * max(0, self.last_pad - len(self.last))
         add("last", last, 0)
+        # mask ids right after `last` (a fixed offset for a captured graph too)
+        add("last_mask", list(self.last_mask) + [-1] * (len(last) - len(self.last_mask)), 0)
         add("new", self.new, L.NEW_FIELDS)
         add("segs", self.segs, L.SEG_FIELDS)
         add("dec", self.dec, L.DEC_FIELDS)

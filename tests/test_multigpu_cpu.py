@@ -26,7 +26,7 @@ def _worker(rank, world, port, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import bench
     from oracle import engine as oe
-    from paper_2507_16784_b200.structure import StructureScanner
+    from paper_2507_16784_b200.grammar import Grammar
     from paper_2507_16784_b200.tokenizer import build_tokenizer
     from paper_2507_16784_b200.traces import make_trace_from_text
     from paper_2507_16784_b200.traces import load_corpus
@@ -40,7 +40,7 @@ def _worker(rank, world, port, out):
                     pool_pages=per * 1600, tokenize=tok.tokenize)
     for i, d in enumerate(docs):
         t = make_trace_from_text(d)
-        sc = StructureScanner(tok)
+        sc = Grammar(t.tool_names, 16, tok).tracker()
         evs, stream, call = {}, [], 0
         for tid in t.script:
             for e in sc.feed(tid):

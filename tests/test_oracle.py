@@ -218,7 +218,7 @@ def test_oracle_engine_matches_reference_bench_config(golden):
     import gzip as _gz
     import json as _json
     from paper_2507_16784_b200.checksum import host_hash, seq_hash_np
-    from paper_2507_16784_b200.structure import StructureScanner
+    from paper_2507_16784_b200.grammar import Grammar
     from paper_2507_16784_b200.traces import load_corpus, make_trace_from_text
     with _gz.open(golden / "bench_runs.json.gz", "rt") as f:
         meta = next(s for s in _json.load(f)["scenarios"] if s["name"] == "c2_g1_r0")
@@ -231,7 +231,7 @@ def test_oracle_engine_matches_reference_bench_config(golden):
                     max_output_tokens=cfg["max_output_tokens"], tokenize=tok.tokenize)
     for d, prompt in zip(meta["docs"], meta["prompts"]):
         t = make_trace_from_text(docs[d])
-        sc, evs, stream, call = StructureScanner(tok), [], [], 0
+        sc, evs, stream, call = Grammar(t.tool_names, 16, tok).tracker(), [], [], 0
         for tid in t.script:
             for e in sc.feed(tid):
                 evs.append([e.kind, len(stream), e.depth, e.payload])

@@ -1,4 +1,4 @@
-"""Tokenizer and structure scanner vs the reference (golden vectors made by
+"""Tokenizer and the native grammar tracker's events vs the reference (golden vectors made by
 oracle/gen_golden.py from threadrun's tokenizer.py and tracker.py)."""
 
 import gzip
@@ -6,7 +6,8 @@ import json
 
 import pytest
 
-from paper_2507_16784_b200.structure import Rejected, StructureScanner
+from paper_2507_16784_b200.grammar import Grammar
+from paper_2507_16784_b200.structure import Rejected
 from paper_2507_16784_b200.tokenizer import build_tokenizer
 
 
@@ -28,7 +29,7 @@ def test_events_match_reference_tracker(golden):
     recs = _load(golden, "events.json.gz")
     assert len(recs) > 150
     for rec in recs:
-        sc = StructureScanner(tok)
+        sc = Grammar(rec["tool_names"], 16, tok).tracker()
         got = []
         for t in rec["stream"]:
             got.extend([e.kind, e.offset, e.depth, e.payload] for e in sc.feed(t))
@@ -45,8 +46,8 @@ def test_stream_equals_document_tokens(golden):
 def test_rejects_non_document():
     tok = build_tokenizer()
     with pytest.raises(Rejected):
-        StructureScanner(tok).feed(ord("x"))
-    sc = StructureScanner(tok)
+        Grammar([], 16, tok).tracker().feed(ord("x"))
+    sc = Grammar([], 16, tok).tracker()
     for t in tok.tokenize('[{"thought":"a","conclusion":"b"}]'):
         sc.feed(t)
     assert sc.done
@@ -74,6 +75,6 @@ def test_deep_doc_structure_matches_reference_shape(golden):
         _, levels, branching, seed = rec["gen"]
         tr = make_trace_from_text(deep_recursion_doc(levels, branching, seed=seed + 100))
         assert len(tr.script) == len(rec["script"])
-        sc = StructureScanner(tok)
+        sc = Grammar(tr.tool_names, 16, tok).tracker()
         got = [[e.kind, e.offset, e.depth, e.payload] for t in tr.script for e in sc.feed(t)]
         assert got == rec["events"]

@@ -101,6 +101,20 @@ int32_t tim_pool_init(int32_t* free_stack, int32_t* owner, int32_t capacity, voi
 int32_t tim_page_ops(const int32_t* step, int32_t* free_stack, int32_t* owner, int32_t capacity,
                      int32_t* block_tables, int64_t table_stride, int32_t* err, void* stream);
 
+/* StepReport / RequestMetrics from device counters (scheduler.py:320-335,513-519;
+ * pruning.py:36-58).  After a step's page ops and row staging: replay the op
+ * list against the pool's device free-stack pointer acct[0] (a host-planned
+ * sp_before that disagrees raises TIM_DOUBLE_FREE), count steps in acct[1]
+ * (acct starts as {capacity, 0}); with slot_acct ([2][n_slots], zeroed), keep
+ * every slot's table length and high-water mark (max_cache, taken at each
+ * ALLOC as _touch_memory does after each forward), count the step's
+ * first-encoded rows per slot and their flops units sum(position+1)
+ * (scheduler.py:374-377), and write the record {serial, pages_free, flops_lo,
+ * flops_hi, (len, decoded, max_cache) x n_slots} to ring entry
+ * (acct[1] - 1) % ring_cap of `reports` (NULL: no record). */
+int32_t tim_step_account(const int32_t* step, int32_t* acct, int32_t* slot_acct, int32_t n_slots,
+                         int32_t* reports, int32_t ring_cap, int32_t* err, void* stream);
+
 /* -------------------------------------------------------- subtask prune (K4) */
 /* For each prune job: verify suffix_start against live[] (the first index with
  * live >= reencode_from, pruning.py:126-128), mark retained entries of

@@ -64,6 +64,7 @@ SIGNATURES = {
     "tim_gemm_ws_floats": (_i64, [_i32, _i32]),
     "tim_gemm_skinny": (_i32, [_p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _i32, _p]),
     "tim_gemm_trace": (_i32, [_i32, _p, _i32]),
+    "tim_step_account": (_i32, [_p, _p, _p, _i32, _p, _i32, _p, _p]),
     "tim_masked_argmax": (_i32, [_p, _i32, _i32, _p, _p, _i32, _p, _i32, _p]),
     # grammar tracker (host)
     "tim_grammar_create": (_p, [_p, _p, _i32, _p, _p, _i32, _i32]),

@@ -14,6 +14,15 @@ void set_last_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+void prefer_shared_carveout(const void* kern) {
+  static const void* done[64];
+  static int n = 0;
+  for (int i = 0; i < n; ++i)
+    if (done[i] == kern) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (n < 64) done[n++] = kern;
+}
+
 int32_t check_launch(const char* what) {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

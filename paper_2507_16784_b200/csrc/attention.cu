@@ -837,9 +837,11 @@ __global__ void attn_generic_kernel(const int32_t* __restrict__ step, const T* _
 
 // Split tiles are merged by a CTA that spins on the other pieces' counter
 // (K6).  That is deadlock-free only if every CTA of the grid can be resident at
-// once (the kernels never trigger their dependents early, so no later launch
-// can take the slots a waited-on CTA needs); refuse a grid larger than the
-// device's co-residency capacity for the kernel's threads and shared memory.
+// once: a dependent grid can start only after every CTA of this one has run
+// its griddepcontrol.launch_dependents (the first instruction), i.e. is already
+// resident, so nothing launched later takes a slot a waited-on CTA needs.
+// Refuse a grid larger than the device's co-residency capacity for the
+// kernel's threads and shared memory.
 template <class Kern>
 int32_t check_coresident(Kern kern, int threads, int smem, int n_ctas, int* cap, const char* name) {
   if (*cap <= 0) {
@@ -980,6 +982,7 @@ extern "C" int64_t tim_decode_ws_floats(int32_t n_ctas, int32_t max_dec, int32_t
 extern "C" int32_t tim_attn_plan(const int32_t* step, const int32_t* block_tables, int64_t table_stride,
                                  int32_t n_ctas, int32_t max_dec, int32_t head_dim, float* ws, void* stream) {
   if (n_ctas <= 0 || n_ctas > kPlanMaxCtas) return TIM_OK;   // K1 falls back to its own search
+  prefer_shared(attn_plan_kernel);
   attn_plan_kernel<<<(n_ctas + 7) / 8, 256, 0, (cudaStream_t)stream>>>(step, block_tables, table_stride,
                                                                        n_ctas, max_dec, head_dim, ws);
   return check_launch("attn_plan");

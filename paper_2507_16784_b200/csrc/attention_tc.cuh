@@ -104,6 +104,17 @@ TIM_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   return ok != 0;
 }
+TIM_DEV void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+// ex2.approx without `volatile`, so the compiler may interleave the 64
+// exponentials of a row with the surrounding FMA-pipe work
+TIM_DEV float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 TIM_DEV void tld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 TIM_DEV void tst_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -390,8 +401,8 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
         uint32_t pk[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float p0 = fast_exp2(fmaf(s[2 * i], scale_log2, -msub));
-          const float p1 = fast_exp2(fmaf(s[2 * i + 1], scale_log2, -msub));
+          const float p0 = ex2f(fmaf(s[2 * i], scale_log2, -msub));
+          const float p1 = ex2f(fmaf(s[2 * i + 1], scale_log2, -msub));
           sq[i & 3] += p0 + p1;
           pk[i] = pack_bf16(p0, p1);
         }
@@ -415,10 +426,10 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
           }
           tst_wait();
         }
-        uint8_t* prow = sP + (b * QBLK + qblk) * P_BYTES;
+        const uint32_t prow = smem_u32(sP) + (uint32_t)((b * QBLK + qblk) * P_BYTES);
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<uint4*>(prow + swz(t, c)) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+          st_shared_v4(prow + swz(t, c), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         fence_proxy_async();
         fence_before();
         mbar_arrive(&p_ready[b]);

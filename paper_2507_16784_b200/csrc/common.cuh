@@ -157,4 +157,15 @@ TIM_DEV float warp_max(float v) {
 namespace tim {
 void set_last_error(const char* fmt, ...);
 int32_t check_launch(const char* what);
+
+// Every small kernel of a step asks for the max-shared carveout.  A kernel
+// with little or no shared memory otherwise lets the SMs switch to a large-L1
+// configuration, and the ~200 KB-per-CTA attention launch that follows it has
+// to switch them back: measured on B200 (tools/carveout_probe.py), an empty
+// 148 x 320 grid with 203 KB of dynamic smem bracketed by CUDA events takes
+// 10.2 us after a 0-smem kernel and 6.1 us after any kernel that kept the
+// shared carveout.  Idempotent, once per kernel.
+void prefer_shared_carveout(const void* kern);
+template <typename K>
+inline void prefer_shared(K kern) { prefer_shared_carveout(reinterpret_cast<const void*>(kern)); }
 }  // namespace tim

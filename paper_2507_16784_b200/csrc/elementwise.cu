@@ -313,6 +313,7 @@ using namespace tim;
 // before touching its outputs.
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t st, Args... args) {
+  prefer_shared(kern);
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
@@ -373,7 +374,7 @@ extern "C" int32_t tim_silu_rms(void* u, int32_t n_rows, int32_t width, const vo
 extern "C" int32_t tim_embed(const int32_t* row_tokens, int32_t n_rows, const void* emb, int32_t dm,
                              void* h, int32_t dtype, void* stream) {
   if (n_rows <= 0) return TIM_OK;
-  TIM_DISPATCH(dtype, embed_kernel<T><<<n_rows, 256, 0, (cudaStream_t)stream>>>(
+  TIM_DISPATCH(dtype, prefer_shared(embed_kernel<T>); embed_kernel<T><<<n_rows, 256, 0, (cudaStream_t)stream>>>(
                           row_tokens, (const T*)emb, dm, (T*)h));
   return check_launch("embed");
 }
@@ -381,7 +382,7 @@ extern "C" int32_t tim_embed(const int32_t* row_tokens, int32_t n_rows, const vo
 extern "C" int32_t tim_rmsnorm(const void* x, int64_t x_stride, void* y, int64_t y_stride,
                                int32_t n_rows, int32_t dm, float eps, int32_t dtype, void* stream) {
   if (n_rows <= 0) return TIM_OK;
-  TIM_DISPATCH(dtype, rmsnorm_kernel<T><<<n_rows, 512, 0, (cudaStream_t)stream>>>(
+  TIM_DISPATCH(dtype, prefer_shared(rmsnorm_kernel<T>); rmsnorm_kernel<T><<<n_rows, 512, 0, (cudaStream_t)stream>>>(
                           (const T*)x, x_stride, (T*)y, y_stride, dm, eps));
   return check_launch("rmsnorm");
 }
@@ -390,7 +391,7 @@ extern "C" int32_t tim_silu(void* x, int64_t n, int32_t dtype, void* stream) {
   if (n <= 0) return TIM_OK;
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  TIM_DISPATCH(dtype, silu_kernel<T><<<(int)blocks, 256, 0, (cudaStream_t)stream>>>((T*)x, n));
+  TIM_DISPATCH(dtype, prefer_shared(silu_kernel<T>); silu_kernel<T><<<(int)blocks, 256, 0, (cudaStream_t)stream>>>((T*)x, n));
   return check_launch("silu");
 }
 
@@ -398,7 +399,7 @@ extern "C" int32_t tim_argmax(const void* logits, int32_t n_rows, int32_t vocab,
                               int32_t dtype, void* stream) {
   if (n_rows <= 0) return TIM_OK;
   const int blocks = (n_rows * 32 + 255) / 256;
-  TIM_DISPATCH(dtype, argmax_kernel<T><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+  TIM_DISPATCH(dtype, prefer_shared(argmax_kernel<T>); argmax_kernel<T><<<blocks, 256, 0, (cudaStream_t)stream>>>(
                           (const T*)logits, n_rows, vocab, out, nullptr, nullptr, 0));
   return check_launch("argmax");
 }
@@ -409,7 +410,7 @@ extern "C" int32_t tim_masked_argmax(const void* logits, int32_t n_rows, int32_t
   if (n_rows <= 0) return TIM_OK;
   if (!mask_ids || !masks || words <= 0) return TIM_BAD_ARGUMENT;
   const int blocks = (n_rows * 32 + 255) / 256;
-  TIM_DISPATCH(dtype, argmax_kernel<T><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+  TIM_DISPATCH(dtype, prefer_shared(argmax_kernel<T>); argmax_kernel<T><<<blocks, 256, 0, (cudaStream_t)stream>>>(
                           (const T*)logits, n_rows, vocab, out, mask_ids, masks, words));
   return check_launch("masked_argmax");
 }

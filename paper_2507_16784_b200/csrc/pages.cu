@@ -176,6 +176,75 @@ __global__ void stage_rows_kernel(const int32_t* step, const int32_t* tables, in
   }
 }
 
+
+// StepReport / RequestMetrics from device counters (scheduler.py:320-335,
+// 513-519; pruning.py:36-58).  Runs after the step's page ops and row staging:
+// replays the op list against the device's own free-stack pointer (acct[0]) --
+// an op whose host-planned sp_before disagrees raises TIM_DOUBLE_FREE -- keeps
+// every slot's table length and high-water mark (max_cache, taken at each
+// ALLOC as _touch_memory does after each forward), and counts the step's
+// first-encoded rows (`new` records staged as rows): decoded tokens per slot
+// and flops units sum(position + 1) (scheduler.py:374-377).  The record lands
+// in a device ring, so reading metrics never synchronises the step.
+__global__ void __launch_bounds__(256) step_account_kernel(const int32_t* step, int32_t* acct, int32_t* slot_acct,
+                                                           int32_t n_slots, int32_t* reports, int32_t ring_cap,
+                                                           int32_t* err) {
+  const tim_step_header& h = *reinterpret_cast<const tim_step_header*>(step);
+  if (slot_acct == nullptr) n_slots = 0;
+  int32_t* slot_len = slot_acct;
+  int32_t* slot_hw = slot_acct + n_slots;
+  __shared__ unsigned long long flops;
+  extern __shared__ int32_t sdec[];
+  for (int i = threadIdx.x; i < n_slots; i += blockDim.x) sdec[i] = 0;
+  if (threadIdx.x == 0) flops = 0ull;
+  __syncthreads();
+  const int32_t* nw = step + h.off_new;
+  for (int i = threadIdx.x; i < h.n_new; i += blockDim.x) {
+    const int32_t* r = nw + (int64_t)i * TIM_NEW_FIELDS;
+    if (r[3] < 0) continue;                      // logged, not encoded this step
+    if (r[0] < n_slots) atomicAdd(&sdec[r[0]], 1);
+    atomicAdd(&flops, (unsigned long long)(r[4] + 1));
+  }
+  if (threadIdx.x == 0) {
+    const int32_t* ops = step + h.off_ops;
+    int32_t sp = acct[0];
+    for (int o = 0; o < h.n_ops; ++o) {
+      const int32_t* op = ops + (int64_t)o * TIM_OP_FIELDS;
+      const int32_t kind = op[0], slot = op[1], toff = op[2], count = op[3], sp_before = op[4];
+      if (sp_before != sp) raise_error(err, TIM_DOUBLE_FREE, -3);
+      sp += kind == TIM_OP_ALLOC ? -count : count;
+      if (slot < n_slots) {
+        if (kind == TIM_OP_ALLOC) {
+          // a table only restarts at index 0 for a new request in the slot
+          // (prompt tokens and the task's opening tokens are never pruned)
+          if (toff == 0) slot_hw[slot] = 0;
+          slot_len[slot] = toff + count;
+          if (toff + count > slot_hw[slot]) slot_hw[slot] = toff + count;
+        } else {
+          slot_len[slot] = toff;
+        }
+      }
+    }
+    acct[0] = sp;
+    acct[1] += 1;
+  }
+  __syncthreads();
+  if (reports == nullptr || ring_cap <= 0) return;
+  const int rec_len = 4 + 3 * n_slots;
+  int32_t* rec = reports + (int64_t)((acct[1] - 1) % ring_cap) * rec_len;
+  if (threadIdx.x == 0) {
+    rec[0] = h.serial;
+    rec[1] = acct[0];
+    rec[2] = (int32_t)(flops & 0xffffffffull);
+    rec[3] = (int32_t)(flops >> 32);
+  }
+  for (int i = threadIdx.x; i < n_slots; i += blockDim.x) {
+    rec[4 + 3 * i] = slot_len[i];
+    rec[5 + 3 * i] = sdec[i];
+    rec[6 + 3 * i] = slot_hw[i];
+  }
+}
+
 }  // namespace tim
 
 using namespace tim;
@@ -191,6 +260,7 @@ extern "C" int32_t tim_pool_init(int32_t* free_stack, int32_t* owner, int32_t ca
 extern "C" int32_t tim_page_ops(const int32_t* step, int32_t* free_stack, int32_t* owner,
                                 int32_t capacity, int32_t* block_tables, int64_t table_stride,
                                 int32_t* err, void* stream) {
+  prefer_shared(page_ops_kernel);
   page_ops_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(step, free_stack, owner, capacity,
                                                          block_tables, table_stride, err);
   return check_launch("page_ops");
@@ -201,6 +271,7 @@ extern "C" int32_t tim_prune_compact(const int32_t* step, int32_t max_jobs, int3
                                      int64_t logical_stride, int32_t* row_tokens, int32_t* err,
                                      void* stream) {
   if (max_jobs <= 0) return TIM_OK;
+  prefer_shared(prune_compact_kernel);
   prune_compact_kernel<<<max_jobs, 256, 0, (cudaStream_t)stream>>>(step, live, live_stride, logical,
                                                                    logical_stride, row_tokens, err);
   return check_launch("prune_compact");
@@ -211,9 +282,20 @@ extern "C" int32_t tim_stage_rows(const int32_t* step, const int32_t* block_tabl
                                   int32_t* logical, int64_t logical_stride, int32_t* row_tokens,
                                   int32_t* row_pages, int32_t* row_pos, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  prefer_shared(stage_new_kernel);
   stage_new_kernel<<<16, 256, 0, st>>>(step, live, live_stride, logical, logical_stride, row_tokens);
   int32_t rc = check_launch("stage_new");
   if (rc) return rc;
+  prefer_shared(stage_rows_kernel);
   stage_rows_kernel<<<16, 256, 0, st>>>(step, block_tables, table_stride, row_tokens, row_pages, row_pos);
   return check_launch("stage_rows");
+}
+
+extern "C" int32_t tim_step_account(const int32_t* step, int32_t* acct, int32_t* slot_acct, int32_t n_slots,
+                                    int32_t* reports, int32_t ring_cap, int32_t* err, void* stream) {
+  if (n_slots < 0 || n_slots > 8192) { set_last_error("n_slots out of range"); return TIM_BAD_ARGUMENT; }
+  prefer_shared(step_account_kernel);
+  step_account_kernel<<<1, 256, (size_t)(n_slots > 0 ? n_slots : 1) * sizeof(int32_t), (cudaStream_t)stream>>>(
+      step, acct, slot_acct, n_slots, reports, ring_cap, err);
+  return check_launch("step_account");
 }

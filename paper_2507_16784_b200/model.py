@@ -178,6 +178,13 @@ class StepRuntime:
         self.mask_words = (getattr(model, "vocab_size", 512) + 31) // 32 if model is not None else 16
         self.masks = torch.zeros((self.MASK_CAP, self.mask_words), dtype=torch.int32, device=self.dev)
         self.n_masks = 0
+        # StepReport / metrics from device counters (tim_step_account): per slot
+        # table length + high-water mark, and a ring of per-descriptor records
+        self.slot_acct = torch.zeros(2 * max(max_slots, 1), dtype=torch.int32, device=self.dev)
+        self.reports = torch.zeros((self.REPORT_RING, 4 + 3 * max(max_slots, 1)), dtype=torch.int32,
+                                   device=self.dev)
+
+    REPORT_RING = 1024
 
     MASK_CAP = 1 << 14
 
@@ -330,6 +337,10 @@ class StepRuntime:
                    self.logical.shape[1], self.row_tokens.data_ptr(), self.row_pages.data_ptr(),
                    self.row_pos.data_ptr(), st)
             self.launches += 2
+        if sd.ops or sd.new or sd.n_rows:
+            self.pool.account(step, self.slot_acct if self.max_slots > 0 else None,
+                              self.reports if self.max_slots > 0 else None)
+            self.launches += 1
         if pev is not None:
             p1 = torch.cuda.Event(enable_timing=True)
             p1.record()
@@ -356,6 +367,21 @@ class StepRuntime:
 
     def check(self) -> None:
         self.pool.check()
+
+    def device_reports(self) -> list[dict]:
+        """The device's per-descriptor records still in the ring, oldest first:
+        {serial, pages_free, flops_units, slots: [(table_len, decoded, max_cache)]}."""
+        acct = self.pool.acct.cpu().tolist()
+        n = acct[1]
+        ring = self.reports.cpu().numpy()
+        out = []
+        for k in range(max(0, n - self.REPORT_RING), n):
+            r = ring[k % self.REPORT_RING]
+            S = (r.size - 4) // 3
+            out.append({"serial": int(r[0]), "pages_free": int(r[1]),
+                        "flops_units": int(r[2]) & 0xFFFFFFFF | (int(r[3]) << 32),
+                        "slots": r[4:4 + 3 * S].reshape(S, 3).tolist()})
+        return out
 
 
 class B200Transformer:

@@ -58,6 +58,8 @@ class DevicePagePool:
         self.free_stack = torch.empty(capacity, dtype=torch.int32, device=self.device)
         self.owner = torch.empty(capacity, dtype=torch.int32, device=self.device)
         self.err = torch.zeros(2, dtype=torch.int32, device=self.device)
+        # device free-stack pointer + executed-descriptor count (tim_step_account)
+        self.acct = torch.tensor([capacity, 0], dtype=torch.int32, device=self.device)
         L.call("tim_pool_init", self.free_stack.data_ptr(), self.owner.data_ptr(), capacity,
                stream_handle())
         self._sp = self.capacity
@@ -141,6 +143,17 @@ class DevicePagePool:
             self._mirror_valid = False
         L.call("tim_page_ops", step_dev.data_ptr(), self.free_stack.data_ptr(),
                self.owner.data_ptr(), self.capacity, tables.data_ptr(), tables.shape[1],
+               self.err.data_ptr(), stream_handle())
+        if _percall:
+            self.account(step_dev)
+
+    def account(self, step_dev: torch.Tensor, slot_acct: torch.Tensor | None = None,
+                reports: torch.Tensor | None = None) -> None:
+        """Device counters of one executed descriptor (tim_step_account)."""
+        n_slots = 0 if slot_acct is None else slot_acct.numel() // 2
+        L.call("tim_step_account", step_dev.data_ptr(), self.acct.data_ptr(),
+               None if slot_acct is None else slot_acct.data_ptr(), n_slots,
+               None if reports is None else reports.data_ptr(), 0 if reports is None else reports.shape[0],
                self.err.data_ptr(), stream_handle())
 
     def check(self) -> None:

@@ -525,3 +525,38 @@ def test_logical_stream_grows_past_engine_cap():
         assert eng.result(rid)["status"] == "finished"
         assert eng.result(rid)["text"] == doc
     assert eng.runtime.logical.shape[1] > cap0
+
+
+def test_device_step_reports_match_reference_runs(golden):
+    """every step's StepReport fields and the requests'
+    max_cache as the DEVICE counts them (tim_step_account: its own free-stack
+    pointer, block-table lengths and high-water marks, staged first-encoded
+    rows) equal the reference Engine's (scheduler.py:320-335, 513-519)."""
+    scens = _load(golden, "engine_runs.json.gz")
+    checked = 0
+    for scen in scens:
+        eng, rids = _engine_for(scen)
+        active = set()
+        for gs in scen["steps"]:
+            rep = eng.step()
+            dev = eng.device_step_report()
+            where = (scen["name"], rep.step)
+            assert dev["pages_free"] == gs["report"][5], where
+            assert dev["flops_units"] == gs["report"][6], where
+            assert {r: v for r, v in dev["request_live"].items() if v} == \
+                {r: v for r, v in gs["request_live"].items() if v}, where
+            want = {}
+            for rid in eng.requests:
+                n = gs["decoded"].get(rid, 0)
+                if rid not in active and dev["request_live"].get(rid, 0) + n > 0 and \
+                        eng.requests[rid].status.value != "queued":
+                    n += len(eng.requests[rid].prompt_tokens)      # activated: prompt rows
+                    active.add(rid)
+                if n:
+                    want[rid] = n
+            got = dev["first_encoded"]
+            assert {r: v for r, v in got.items() if r in want or v} == want, where
+            for rid, v in dev["max_cache"].items():
+                assert v == eng.requests[rid].metrics.max_cache, (where, rid)
+            checked += 1
+    assert checked > 1000

@@ -50,6 +50,9 @@ enum {
 /* Header of the per-step descriptor.  Offsets are int32 element offsets into
  * the same buffer.  Record layouts (int32 fields):
  *   new   : {slot, logical_idx, token, row, live_idx}          host-known tokens
+ *           (row -1: logged, not encoded; -2: counted by tim_step_account only)
+ *   last  : rows whose logits are produced, then last_mask: one mask id per
+ *           `last` entry for tim_masked_argmax (-1: unmasked)
  *   seg   : {slot, m, n, row_off}                               one encode segment
  *   dec   : {row, slot, kv_len, nq, m, group} + dec_prefix[n_dec+1]
  *                                   decode tiles (1 query x all kv heads; m = first fresh key)

@@ -143,6 +143,7 @@ __global__ void stage_new_kernel(const int32_t* step, int32_t* live, int64_t lst
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < h.n_new; i += gridDim.x * blockDim.x) {
     const int32_t* r = nw + (int64_t)i * TIM_NEW_FIELDS;
     const int32_t slot = r[0], lidx = r[1], tok = r[2], row = r[3], live_idx = r[4];
+    if (row == -2) continue;                   // counted by the step report only
     logical[(int64_t)slot * gstride + lidx] = tok;
     if (row >= 0) {
       live[(int64_t)slot * lstride + live_idx] = lidx;
@@ -201,8 +202,10 @@ __global__ void __launch_bounds__(256) step_account_kernel(const int32_t* step, 
   const int32_t* nw = step + h.off_new;
   for (int i = threadIdx.x; i < h.n_new; i += blockDim.x) {
     const int32_t* r = nw + (int64_t)i * TIM_NEW_FIELDS;
-    if (r[3] < 0) continue;                      // logged, not encoded this step
-    if (r[0] < n_slots) atomicAdd(&sdec[r[0]], 1);
+    if (r[3] == -1) continue;                    // logged, not encoded this step
+    // row -2: first-encoded by the reference's forward, not staged here (its
+    // request ended this step): flops units only
+    if (r[3] >= 0 && r[0] < n_slots) atomicAdd(&sdec[r[0]], 1);
     atomicAdd(&flops, (unsigned long long)(r[4] + 1));
   }
   if (threadIdx.x == 0) {

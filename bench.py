@@ -228,15 +228,22 @@ def run_gpu(args, rank: int, world: int, dist):
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
     clocks.start()
     barrier()
+    # TIMRUN_PROFILE_TIMED=1 brackets each timed step with cudaProfilerStart/Stop
+    # (ncu --profile-from-start off then captures exactly the value window)
+    prof = os.environ.get("TIMRUN_PROFILE_TIMED") == "1"
     for i, (sd, step, fw) in enumerate(resident):
         if i in timed_set:
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             rt.attn_events = attn_store
             l0 = rt.launches
+            if prof:
+                torch.cuda.cudart().cudaProfilerStart()
             a.record()
             rt._execute(sd, step, fw)
             b.record()
+            if prof:
+                torch.cuda.cudart().cudaProfilerStop()
             rt.attn_events = None
             launches_timed += rt.launches - l0
             step_ev.append((a, b, i))

@@ -225,28 +225,6 @@ int32_t tim_attn_extend(const int32_t* step, int32_t max_items, const void* q, v
                         int64_t table_stride, int32_t hq, int32_t hkv, int32_t head_dim,
                         float scale, int32_t dtype, void* stream);
 
-/* ---------------------------------------------------- skinny decode GEMM */
-/* 2D bf16 TMA tensor map (row-major [rows, cols], 128B swizzle, box
- * box_rows x box_cols with box_cols*2 == 128) written to tmap_out (128 bytes,
- * host memory). */
-int32_t tim_tmap_2d_bf16(void* tmap_out, const void* base, int64_t rows, int64_t cols,
-                         int32_t box_rows, int32_t box_cols);
-/* Y[M,N] = (R +) X[M,K] . Wt[N,K]^T for M <= 64 decode rows (the q/k/v, o,
- * up and down projections of model.py:143-161 at decode batch sizes):
- * tcgen05 MMA (128 weight rows x 64 activation rows per tile, TMEM
- * accumulators), stream-K over (128-column x 128-k) chunks with TMA tile
- * loads and an in-kernel split merge.  tmap_x: X with 64x64 boxes; tmap_w:
- * Wt with 128x64 boxes; R may alias Y (in-place residual add).  ws
- * (tim_gemm_ws_floats floats) and counters (int32[N/128]) are zero-initialised
- * once and left zeroed by every launch. */
-int64_t tim_gemm_ws_floats(int32_t n_ctas, int32_t n);
-int32_t tim_gemm_skinny(const void* tmap_x, const void* tmap_w, void* y, const void* res, int32_t M,
-                        int32_t N, int32_t K, float* ws, int32_t* counters, int32_t n_ctas,
-                        void* stream);
-/* Diagnostics: on != 0 makes tim_gemm_skinny record per-CTA phase
- * timestamps; out (host, n uint64) receives the last launch's record. */
-int32_t tim_gemm_trace(int32_t on, uint64_t* out, int32_t n);
-
 /* Greedy argmax over rows of logits [n, vocab] (lowest id on ties, model.py:186-192). */
 int32_t tim_argmax(const void* logits, int32_t n_rows, int32_t vocab, int32_t* out,
                    int32_t dtype, void* stream);

@@ -60,10 +60,6 @@ SIGNATURES = {
     "tim_tc_trace": (_i32, [_p]),
     "tim_noop": (_i32, [_i32, _i32, _i32, _p]),
     "tim_attn_plan": (_i32, [_p, _p, _i64, _i32, _i32, _i32, _p, _p]),
-    "tim_tmap_2d_bf16": (_i32, [_p, _p, _i64, _i64, _i32, _i32]),
-    "tim_gemm_ws_floats": (_i64, [_i32, _i32]),
-    "tim_gemm_skinny": (_i32, [_p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _i32, _p]),
-    "tim_gemm_trace": (_i32, [_i32, _p, _i32]),
     "tim_step_account": (_i32, [_p, _p, _p, _i32, _p, _i32, _p, _p]),
     "tim_masked_argmax": (_i32, [_p, _i32, _i32, _p, _p, _i32, _p, _i32, _p]),
     # grammar tracker (host)

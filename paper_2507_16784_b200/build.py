@@ -14,7 +14,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtimrun.so"
-SOURCES = ["abi.cu", "pages.cu", "elementwise.cu", "attention.cu", "gemm.cu", "grammar.cpp"]
+SOURCES = ["abi.cu", "pages.cu", "elementwise.cu", "attention.cu", "grammar.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -430,13 +430,6 @@ class B200Transformer:
         self.wo = [w.t() for w in self.wo_t]
         self.w1 = [w.t() for w in self.w1_t]
         self.w2 = [w.t() for w in self.w2_t]
-        # weight-streaming decode GEMM (tim_gemm_skinny) for steps of <= 64 rows
-        W = (hq + 2 * hkv) * D
-        self.skinny = (cfg.precision == "bfloat16" and os.environ.get("TIMRUN_SKINNY", "0") == "1"
-                       and all(n % 128 == 0 for n in (W, dm, cfg.n_mlp)))
-        if self.skinny:
-            self.tmaps = [[self._tmap(w, 128) for w in (self.wqkv_t[li], self.wo_t[li], self.w1_t[li],
-                                                   self.w2_t[li])] for li in range(cfg.layers)]
         self.emb_t = self.emb.t().contiguous()     # tied LM head (model.py:164)
         cos, sin = _rope_tables(cfg)
         self.cos = torch.from_numpy(cos).to(self.dev)
@@ -453,31 +446,17 @@ class B200Transformer:
         self.ext_groups = L.load().tim_extend_head_groups(hq, hkv, D) if self.ext_q else 0
         self._runtimes: dict[int, StepRuntime] = {}
 
-    @staticmethod
-    def _tmap(t: torch.Tensor, box_rows: int = 64):
-        """128-byte TMA descriptor of a row-major bf16 matrix, boxes of box_rows x 64."""
-        buf = (ctypes.c_uint8 * 128)()
-        L.call("tim_tmap_2d_bf16", ctypes.addressof(buf), t.data_ptr(), t.shape[0], t.shape[1],
-               box_rows, 64)
-        return buf
-
     # Diagnostics only (bench ablation of kernel classes; results are garbage):
     # TIMRUN_DIAG_SKIP=gemm,rope,silu,attn drops those launches from the step.
     _DIAG_SKIP = frozenset(x for x in os.environ.get("TIMRUN_DIAG_SKIP", "").split(",") if x)
 
     def _gemm(self, rt, li: int, which: int, x, y, res, T: int) -> int:
-        """y (+)= x @ W for projection `which` (0 qkv, 1 o, 2 up, 3 down):
-        the weight-streaming kernel for <= 64 rows, cuBLAS otherwise."""
+        """y (+)= x @ W for projection `which` (0 qkv, 1 o, 2 up, 3 down) on
+        cuBLAS (a tcgen05 weight-streaming kernel for <= 64 rows was measured
+        slower)."""
         if "gemm" in self._DIAG_SKIP:
             return 0
         wt = (self.wqkv_t, self.wo_t, self.w1_t, self.w2_t)[which][li]
-        if self.skinny and T <= 64:
-            N, K = wt.shape
-            L.call("tim_gemm_skinny", ctypes.addressof(rt.x_maps[id(x)]),
-                   ctypes.addressof(self.tmaps[li][which]), y.data_ptr(),
-                   None if res is None else res.data_ptr(), T, N, K, rt.gws.data_ptr(),
-                   rt.gcnt.data_ptr(), rt.sms, stream_handle())
-            return 1
         if res is None:
             torch.matmul(x[:T], wt.t(), out=y[:T])
         else:
@@ -593,12 +572,6 @@ class B200Transformer:
         rt.max_dec = R
         rt.ws = torch.zeros(L.load().tim_decode_ws_floats(n_ctas, R, cfg.n_kv, D), device=d)
         rt.counters = torch.zeros(R * 8, dtype=torch.int32, device=d)
-        if self.skinny:   # decode-GEMM activation descriptors (buffers are fixed) + workspace
-            rt.x_maps = {id(t): self._tmap(t) for t in (rt.h, rt.ctx, rt.u)}
-            rt.gws = torch.zeros(L.load().tim_gemm_ws_floats(n_ctas, max(cfg.n_mlp, dm, (cfg.heads + 2 * cfg.n_kv) * D)),
-                                 device=d)
-            rt.gcnt = torch.zeros(max(cfg.n_mlp, dm, (cfg.heads + 2 * cfg.n_kv) * D) // 64,
-                                  dtype=torch.int32, device=d)
 
     # The forward is split in three phases so that a decode step can run as
     # two captured CUDA graphs around one eagerly launched layer-0 attention

@@ -448,8 +448,11 @@ def cpu_reference(budget_s: float, steps: int, warmup: int, threshold: int, n_re
             break
     est_s = len(calls) * float(np.mean(times))
     value = tokens / est_s
-    # leg 3: the scripted reference Engine (page accounting only) on the same requests
-    acc = scripted_engine_rate(min(budget_s / 3, 10.0), n_req, threshold)
+    # leg 3: the scripted reference Engine (page accounting only) on the same
+    # requests -- the reference's own code when baseline/_ref is installed
+    acc, acc_kind = reference_scripted_rate(min(budget_s / 3, 10.0), n_req, threshold)
+    if acc is None:
+        acc, acc_kind = scripted_engine_rate(min(budget_s / 3, 10.0), n_req, threshold), "port"
     import threadpoolctl
     blas = threadpoolctl.threadpool_info()
     threads = max([b.get("num_threads", 1) for b in blas] or [1])
@@ -460,7 +463,43 @@ def cpu_reference(budget_s: float, steps: int, warmup: int, threshold: int, n_re
                        f"recorded (prefix m, rows n); {sum(times):.1f} s measured, steps' time estimated "
                        f"as #forwards x mean = {est_s:.0f} s for {tokens} tokens; numpy {np.__version__}, "
                        f"BLAS threads {threads}, os.cpu_count {os.cpu_count()}"),
-            "scripted_engine_tokens_per_s": acc}
+            "scripted_engine_tokens_per_s": acc, "scripted_engine_kind": acc_kind}
+
+
+def reference_scripted_rate(budget_s: float, n_req: int, threshold: int):
+    """SURVEY §8d leg 3 on the REFERENCE's own code: threadrun's Engine with its
+    ScriptedModel (scheduler.py:274-442, model.py:195-233; page accounting and
+    grammar tracking, no arithmetic) from baseline/_ref, on the C2 requests,
+    for `budget_s` of host time: (tokens/s, "reference") or (None, None)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "threadrun").is_dir():
+        return None, None
+    sys.path.insert(0, str(ref))
+    try:
+        from threadrun.model import ScriptedModel
+        from threadrun.scheduler import BatchConfig, Engine
+        from threadrun.schema import ToolSpec, parse_tree_text
+        from threadrun.tokenizer import build_tokenizer
+        from threadrun.traces import make_trace
+    finally:
+        sys.path.remove(str(ref))
+    from paper_2507_16784_b200.traces import load_corpus
+    tok = build_tokenizer()
+    P = 40960
+    eng = Engine(ScriptedModel(position_limit=P),
+                 BatchConfig(max_batch=n_req, buffer_threshold=threshold, position_limit=P,
+                             pool_pages=n_req * 1600, max_queue=max(64, n_req), check_masks=False,
+                             max_output_tokens=20000))
+    docs = load_corpus(ROOT / "tests" / "golden" / "corpus_tool_chain32.json.gz")
+    for i in shard_docs(0, 1, n_req):
+        t = make_trace(parse_tree_text(docs[i]), tok)
+        eng.submit(f"q{i}:", [ToolSpec(n) for n in t.tool_names], script=t.script,
+                   tool_responses=t.tool_responses or None)
+    t0 = time.perf_counter()
+    toks = 0
+    while time.perf_counter() - t0 < budget_s and not eng.all_terminal():
+        toks += sum(eng.step().decoded.values())
+    return toks / (time.perf_counter() - t0), "reference"
 
 
 def scripted_engine_rate(budget_s: float, n_req: int, threshold: int) -> float:

@@ -187,6 +187,8 @@ __global__ void stage_rows_kernel(const int32_t* step, const int32_t* tables, in
 // first-encoded rows (`new` records staged as rows): decoded tokens per slot
 // and flops units sum(position + 1) (scheduler.py:374-377).  The record lands
 // in a device ring, so reading metrics never synchronises the step.
+constexpr int kAcctOps = 1024;   // ops staged in shared memory (a longer list runs serially)
+
 __global__ void __launch_bounds__(256) step_account_kernel(const int32_t* step, int32_t* acct, int32_t* slot_acct,
                                                            int32_t n_slots, int32_t* reports, int32_t ring_cap,
                                                            int32_t* err) {
@@ -195,9 +197,23 @@ __global__ void __launch_bounds__(256) step_account_kernel(const int32_t* step, 
   int32_t* slot_len = slot_acct;
   int32_t* slot_hw = slot_acct + n_slots;
   __shared__ unsigned long long flops;
+  __shared__ int32_t sop[kAcctOps][4];       // kind, slot, table_off, count
+  __shared__ int32_t sp_end;
   extern __shared__ int32_t sdec[];
+  const int n_ops = h.n_ops;
+  const int32_t* ops = step + h.off_ops;
   for (int i = threadIdx.x; i < n_slots; i += blockDim.x) sdec[i] = 0;
   if (threadIdx.x == 0) flops = 0ull;
+  const bool staged = n_ops <= kAcctOps;
+  if (staged) {
+    for (int o = threadIdx.x; o < n_ops; o += blockDim.x) {
+      const int32_t* op = ops + (int64_t)o * TIM_OP_FIELDS;
+      sop[o][0] = op[0];
+      sop[o][1] = op[1];
+      sop[o][2] = op[2];
+      sop[o][3] = op[3];
+    }
+  }
   __syncthreads();
   const int32_t* nw = step + h.off_new;
   for (int i = threadIdx.x; i < h.n_new; i += blockDim.x) {
@@ -208,18 +224,53 @@ __global__ void __launch_bounds__(256) step_account_kernel(const int32_t* step, 
     if (r[3] >= 0 && r[0] < n_slots) atomicAdd(&sdec[r[0]], 1);
     atomicAdd(&flops, (unsigned long long)(r[4] + 1));
   }
-  if (threadIdx.x == 0) {
-    const int32_t* ops = step + h.off_ops;
+  if (staged) {
+    // free-stack pointer: warp 0 scans the ops' deltas; every host-planned
+    // sp_before must equal the device's running pointer
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      int32_t sp = acct[0];
+      for (int o0 = 0; o0 < n_ops; o0 += 32) {
+        const int o = o0 + lane;
+        int32_t d = 0;
+        if (o < n_ops) d = sop[o][0] == TIM_OP_ALLOC ? -sop[o][3] : sop[o][3];
+        int32_t inc = d;
+#pragma unroll
+        for (int k = 1; k < 32; k <<= 1) {
+          const int32_t v = __shfl_up_sync(0xffffffffu, inc, k);
+          if (lane >= k) inc += v;
+        }
+        if (o < n_ops && ops[(int64_t)o * TIM_OP_FIELDS + 4] != sp + inc - d) raise_error(err, TIM_DOUBLE_FREE, -3);
+        sp += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) sp_end = sp;
+    }
+    // per slot: its ops in order (table length; high-water mark at each ALLOC,
+    // reset when a table restarts at index 0 for a new request)
+    for (int sl = threadIdx.x; sl < n_slots; sl += blockDim.x) {
+      int32_t len = slot_len[sl], hw = slot_hw[sl];
+      for (int o = 0; o < n_ops; ++o) {
+        if (sop[o][1] != sl) continue;
+        if (sop[o][0] == TIM_OP_ALLOC) {
+          if (sop[o][2] == 0) hw = 0;
+          len = sop[o][2] + sop[o][3];
+          hw = len > hw ? len : hw;
+        } else {
+          len = sop[o][2];
+        }
+      }
+      slot_len[sl] = len;
+      slot_hw[sl] = hw;
+    }
+  } else if (threadIdx.x == 0) {
     int32_t sp = acct[0];
-    for (int o = 0; o < h.n_ops; ++o) {
+    for (int o = 0; o < n_ops; ++o) {
       const int32_t* op = ops + (int64_t)o * TIM_OP_FIELDS;
       const int32_t kind = op[0], slot = op[1], toff = op[2], count = op[3], sp_before = op[4];
       if (sp_before != sp) raise_error(err, TIM_DOUBLE_FREE, -3);
       sp += kind == TIM_OP_ALLOC ? -count : count;
       if (slot < n_slots) {
         if (kind == TIM_OP_ALLOC) {
-          // a table only restarts at index 0 for a new request in the slot
-          // (prompt tokens and the task's opening tokens are never pruned)
           if (toff == 0) slot_hw[slot] = 0;
           slot_len[slot] = toff + count;
           if (toff + count > slot_hw[slot]) slot_hw[slot] = toff + count;
@@ -228,7 +279,11 @@ __global__ void __launch_bounds__(256) step_account_kernel(const int32_t* step, 
         }
       }
     }
-    acct[0] = sp;
+    sp_end = sp;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    acct[0] = sp_end;
     acct[1] += 1;
   }
   __syncthreads();
@@ -237,7 +292,7 @@ __global__ void __launch_bounds__(256) step_account_kernel(const int32_t* step, 
   int32_t* rec = reports + (int64_t)((acct[1] - 1) % ring_cap) * rec_len;
   if (threadIdx.x == 0) {
     rec[0] = h.serial;
-    rec[1] = acct[0];
+    rec[1] = sp_end;
     rec[2] = (int32_t)(flops & 0xffffffffull);
     rec[3] = (int32_t)(flops >> 32);
   }
@@ -247,7 +302,6 @@ __global__ void __launch_bounds__(256) step_account_kernel(const int32_t* step, 
     rec[6 + 3 * i] = slot_hw[i];
   }
 }
-
 }  // namespace tim
 
 using namespace tim;

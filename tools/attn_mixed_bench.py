@@ -121,7 +121,8 @@ def main():
             L.call("tim_tc_trace", None)
             t = tr.view(64, 8).cpu().numpy().astype(np.float64)
             t0 = t[t > 0].min()
-            names = ["prod_slot_free", "prod_published", "mma_kv_full", "mma_p_ready", "sm_s_ready", "sm_p_done"]
+            names = ["prod_slot_free", "pv1_issue", "s0_issue", "pv0_issue", "sm0_s_ready", "sm0_p_done",
+                     "sm1_s_ready", "sm1_p_done"]
             for g in range(64):
                 if t[g, 0] == 0:
                     break

@@ -53,28 +53,36 @@ def timed_window(eng, steps, block=20):
                 prologue_ms=pro_ms)
 
 
-def c2_like(threshold, skip, steps):
+def c2_like(threshold, skip, steps, complete=False):
     # pruning off keeps every token: ~7.1K pages per request at the end
     eng, cfg, model = bench.build_engine(0, 64, threshold,
                                          pool_per_req=7400 if threshold == NO_PRUNING else 1600)
     eng.runtime.precapture()
-    for _ in range(skip):
-        eng.step()
-    w = timed_window(eng, steps)
+    if complete:          # the whole trajectory, every step timed
+        w = dict(ms=0.0, tokens=0, pages_freed=0, prune_jobs=0, kv_tokens=0, prologue_ms=0.0)
+        while not eng.all_terminal():
+            wi = timed_window(eng, 256)
+            for k in w:
+                w[k] += wi[k]
+        steps = eng.step_index
+    else:
+        for _ in range(skip):
+            eng.step()
+        w = timed_window(eng, steps)
     kv_bytes = w["kv_tokens"] * cfg.kv_bytes_per_token() / steps
-    return {"threshold": threshold if threshold != NO_PRUNING else "none",
-            "tokens_per_s": w["tokens"] / (w["ms"] * 1e-3), "ms_per_step": w["ms"] / steps,
+    return {"threshold": threshold if threshold != NO_PRUNING else "none", "steps": steps,
+            "tokens": w["tokens"], "tokens_per_s": w["tokens"] / (w["ms"] * 1e-3), "ms_per_step": w["ms"] / steps,
             "attention_kv_bytes_per_step": kv_bytes,
             "mean_retained_per_request": w["kv_tokens"] / steps / 64}
 
 
 def run_c5(a):
     out = {"config": "C5 ablation: C2 (64 x tool_chain_tree(32), Qwen3-8B shape, bf16) pruning on (T=2) vs off",
-           "skip_steps": a.skip, "steps": a.steps}
+           "window": "whole trajectories, every step timed" if a.complete else f"steps {a.skip}..{a.skip + a.steps}"}
     import paper_2507_16784_b200.model as M  # noqa: F401
-    on = c2_like(2, a.skip, a.steps)
+    on = c2_like(2, a.skip, a.steps, a.complete)
     torch.cuda.empty_cache()
-    off = c2_like(NO_PRUNING, a.skip, a.steps)
+    off = c2_like(NO_PRUNING, a.skip, a.steps, a.complete)
     out.update(on=on, off=off,
                attention_bytes_ratio=on["attention_kv_bytes_per_step"] / off["attention_kv_bytes_per_step"],
                tokens_per_s_ratio=on["tokens_per_s"] / off["tokens_per_s"])

@@ -105,6 +105,13 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def local_device() -> int:
+    """This rank's GPU: LOCAL_RANK (modulo the visible devices, so a smoke
+    test can run several ranks on one GPU)."""
+    import torch
+    return int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1)
+
+
 def reduce_over_ranks(dist, times, counts, device="cpu"):
     """Times: max over ranks (the job ends with its slowest rank); counts: sum."""
     import torch
@@ -185,7 +192,7 @@ def run_gpu(args, rank: int, world: int, dist):
     the step descriptor, device work, D2H), synchronised on both sides."""
     import torch
     from paper_2507_16784_b200.checksum import device_hashes, host_hash, seq_hash_np
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(local_device())
     gold = golden_rows(rank, world, args.threshold, args.batch)
 
     def barrier():
@@ -211,7 +218,8 @@ def run_gpu(args, rank: int, world: int, dist):
     assert len(records) == n_steps, (len(records), n_steps)
     # every rank times the same step indices of its own shard
     if dist is not None:
-        t = torch.tensor([n_steps], device="cuda")
+        t = torch.tensor([n_steps], device="cuda" if os.environ.get("TIMRUN_DIST_BACKEND", "nccl") == "nccl"
+                         else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         n_steps_common = int(t.item())
     else:
@@ -225,7 +233,7 @@ def run_gpu(args, rank: int, world: int, dist):
     attn_store, step_ev = [], []
     launches0 = rt.launches
     launches_timed = 0
-    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
+    clocks = ClockSampler(local_device())
     clocks.start()
     barrier()
     # TIMRUN_PROFILE_TIMED=1 brackets each timed step with cudaProfilerStart/Stop
@@ -366,7 +374,8 @@ def run_gpu(args, rank: int, world: int, dist):
           f"{e2e_s * 1e3:.1f} ms over {e2e_steps} contiguous steps (token checksum {result_sum})",
           file=sys.stderr)
     ms_max, e2e_ms_max, tok_sum, e2e_tok_sum = reduce_over_ranks(
-        dist, [ms, e2e_s * 1e3], [tokens, e2e_tokens], device="cuda")
+        dist, [ms, e2e_s * 1e3], [tokens, e2e_tokens],
+        device="cuda" if os.environ.get("TIMRUN_DIST_BACKEND", "nccl") == "nccl" else "cpu")
     return dict(ms=ms_max, e2e_ms=e2e_ms_max, tokens=tok_sum, e2e_tokens=e2e_tok_sum,
                 n_timed=len(timed), n_steps=n_steps, mixed_timed=mixed_steps,
                 attn=agg(attn), dec=agg(dec), mix=agg(mix), launches=launches_timed, clocks=clk,
@@ -582,9 +591,16 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist_mod
-        local = int(os.environ.get("LOCAL_RANK", 0))
+        local = local_device()
         torch.cuda.set_device(local)
-        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL for the barrier and the max/sum reductions (no collective on the
+        # data path); TIMRUN_DIST_BACKEND=gloo lets several ranks share one GPU
+        # (a smoke test of the N>1 path on a single-GPU box)
+        backend = os.environ.get("TIMRUN_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist_mod.init_process_group(backend)
         dist = dist_mod
     res = run_gpu(args, rank, world, dist)
     if rank == 0:

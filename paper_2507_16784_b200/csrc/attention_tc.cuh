@@ -40,7 +40,7 @@ constexpr int GRP = 4;               // q heads per kv head
 constexpr int M = 128;               // MMA rows per item
 constexpr int BN = 64;               // keys per block
 constexpr int QBLK = 2;              // q-blocks per item: two MMA row tiles share each K/V block
-constexpr int ST = 3;                // K/V ring stages
+constexpr int ST = 5;                // K/V ring stages
 constexpr int Q_SLAB = M * 128;      // 16 KiB
 constexpr int Q_BYTES = 2 * Q_SLAB;  // 32 KiB
 constexpr int P_BYTES = M * 128;     // 16 KiB (128 rows x 64 keys bf16)
@@ -48,7 +48,7 @@ constexpr int KV_SLAB = BN * 128;    // 8 KiB (64 keys x 64 elements)
 constexpr int K_BYTES = 2 * KV_SLAB;
 constexpr int STAGE = 2 * K_BYTES;   // K then V, 32 KiB
 constexpr int BAR_BYTES = 256;
-constexpr int SMEM = 1024 + QBLK * Q_BYTES + 2 * QBLK * P_BYTES + ST * STAGE + BAR_BYTES;
+constexpr int SMEM = 1024 + QBLK * Q_BYTES + ST * STAGE + BAR_BYTES;
 constexpr int THREADS = 10 * 32;     // 8 softmax warps (4 per q-block), MMA, producer
 constexpr int MMA_WARP = 8, PROD_WARP = 9;
 constexpr int TMEM_COLS = 512;       // S[2 buffers][2 q-blocks] (64 cols each) + O[2 q-blocks] (128 cols)
@@ -74,6 +74,15 @@ TIM_DEV void mma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uin
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// D += A * B with A (M x 16, bf16, K-major) read from TMEM: the P tile the
+// softmax stored over its S buffer (lane = row, 2 bf16 per 32-bit column).
+TIM_DEV void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
 TIM_DEV void commit(uint64_t* bar) {
@@ -143,8 +152,7 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                       // [q-block] 32 KiB A tiles
-  uint8_t* sP = sQ + QBLK * Q_BYTES;        // [buffer][q-block] 16 KiB P tiles
-  uint8_t* sKV = sP + 2 * QBLK * P_BYTES;
+  uint8_t* sKV = sQ + QBLK * Q_BYTES;
   uint64_t* kv_full = reinterpret_cast<uint64_t*>(sKV + ST * STAGE);
   uint64_t* kv_empty = kv_full + ST;
   uint64_t* s_ready = kv_empty + ST;   // [2]
@@ -242,7 +250,7 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
     // the next O += P_g V_g (needs the softmax's P_g).  Whichever is ready is
     // issued, so neither waits behind the other's data.
     if (lane == 0) {
-      const uint32_t qa = smem_u32(sQ), pa = smem_u32(sP), kva = smem_u32(sKV);
+      const uint32_t qa = smem_u32(sQ), kva = smem_u32(sKV);
       auto nblk_of = [&](int it) {
         return it < n_items ? (items[(int64_t)it * TIM_EXT_FIELDS + 2] + BN - 1) / BN : 0;
       };
@@ -297,7 +305,7 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
 #pragma unroll
             for (int kk = 0; kk < BN / 16; ++kk)
               if (qblk < p_nqb)
-              mma_ss(tmem + O_COL + qblk * D, desc_sw128(pa + (b * QBLK + qblk) * P_BYTES + kk * 32, 16, 1024),
+              mma_ts(tmem + O_COL + qblk * D, tmem + (uint32_t)((b * QBLK + qblk) * BN + kk * 8),
                      desc_sw128(vb + kk * 2048, KV_SLAB, 1024), kIdescO, (p_j > 0 || kk > 0) ? 1u : 0u);
           commit(&pv_done[b]);
           commit(&kv_empty[p_g % ST]);
@@ -409,8 +417,10 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
         const float sum = (sq[0] + sq[1]) + (sq[2] + sq[3]);
         l_run = l_run * corr + sum;
         m_run = m_use;
-        // O may be rescaled / P buffer b rewritten only once the PV MMAs of
-        // blocks j-1 (O) and j-2 (P buffer b) are done
+        // observe PV_{g-2} (same barrier as this block's PV; long complete) --
+        // P_{g-2} lived in this S buffer and its PV ran before S_g overwrote it
+        // (the tensor pipe runs in issue order); O may be rescaled only once
+        // PV_{g-1} is done
         if (gb >= 2 && j >= 2) mbar_wait(&pv_done[b], ((gb - 2) >> 1) & 1);
         if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
           mbar_wait(&pv_done[b ^ 1], ((gb - 1) >> 1) & 1);
@@ -426,11 +436,15 @@ TIM_DEV void ext_tc_body(const __nv_bfloat16* __restrict__ kl, const __nv_bfloat
           }
           tst_wait();
         }
-        const uint32_t prow = smem_u32(sP) + (uint32_t)((b * QBLK + qblk) * P_BYTES);
+        // P (bf16 pairs) over the first 32 columns of this block's S buffer:
+        // the TMEM A operand of its PV MMA
+        {
+          float pf[32];
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          st_shared_v4(prow + swz(t, c), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-        fence_proxy_async();
+          for (int i = 0; i < 32; ++i) pf[i] = __uint_as_float(pk[i]);
+          tst32(lane_base + (uint32_t)(b * QBLK * BN) + s_col, pf);
+        }
+        tst_wait();
         fence_before();
         mbar_arrive(&p_ready[b]);
         if (threadIdx.x == 0) TCT(5, gb);

@@ -62,17 +62,19 @@ class StepDesc:
         self.jobs.append((slot, old_len, s, reencode_from, off, len(spans), out_row, keep))
 
     # Cost model of the one-launch attention (mode 2), in SM-microseconds,
-    # calibrated on B200 with tools/attn_mixed_bench.py (mode 2, decode CTAs
-    # streaming next to the items) and bench.py's mixed steps: a decode-tile
-    # CTA streams ~40 KB/us of page rows; a multi-token item costs ~3 us (Q
-    # load, epilogue) plus ~1.2 us per 64-key block for each of its (up to two)
-    # 32-query blocks; items are dealt longest-first, round-robin.  (4.0/1.6
-    # over-reserved CTAs for the items: bench mixed launches 66.1 -> 59.6 us;
-    # 2.0/0.8 under-reserves them: 68.7 us.)  TIMRUN_EXT_COST="item,block"
-    # overrides.
-    DEC_US_PER_TOKEN = 4096 / 40e3
+    # calibrated on B200 on bench.py's own mixed steps (tools/split_sweep.py:
+    # every sampled mixed step of the C2 trajectory re-packed under each
+    # candidate and its layer-0 launch timed): a decode-tile CTA streams ~36
+    # KB/us of page rows next to the items; a multi-token item costs ~8 us
+    # (Q load, pipeline fill and drain, epilogue -- items on one CTA run back to
+    # back) plus ~0.8 us per 64-key block for each of its (up to two) 32-query
+    # blocks; items are dealt longest-first, round-robin.  Round-2 sweeps (K2
+    # with P in TMEM and a 5-stage ring): (3.0, 1.2, 40 KB/us) 66.5-69.2 us ->
+    # (8.0, 0.8, 36 KB/us) 63.4-64.6 us per mixed launch (run-to-run noise ~2
+    # us).  TIMRUN_EXT_COST="item,block" overrides.
+    DEC_US_PER_TOKEN = 4096 / 36e3
     EXT_US_PER_ITEM, EXT_US_PER_QBLOCK_BLOCK = (
-        float(x) for x in os.environ.get("TIMRUN_EXT_COST", "3.0,1.2").split(","))
+        float(x) for x in os.environ.get("TIMRUN_EXT_COST", "8.0,0.8").split(","))
 
     def _split_cost(self, ext: list) -> tuple[float, int]:
         """(estimated us, CTAs for the items) of the best split for `ext`."""

@@ -37,7 +37,8 @@ def main():
     timed = set(bench.sampled_steps(len(records), a.steps, 5))
     mixed = [i for i in sorted(timed) if records[i][0].ext][: a.max_mixed]
     resident = rt.replay_upload(records)
-    cands = [(3.0, 1.2, 4096 / 40e3)] + list(itertools.product((4.0, 5.0, 6.0, 8.0), (0.6, 0.8, 1.0, 1.2), (4096 / 36e3, 4096 / 40e3)))
+    base = (StepDesc.EXT_US_PER_ITEM, StepDesc.EXT_US_PER_QBLOCK_BLOCK, StepDesc.DEC_US_PER_TOKEN)
+    cands = [base, (3.0, 1.2, 4096 / 40e3)] + list(itertools.product((10.0, 12.0, 15.0, 20.0), (0.6, 0.7, 0.8, 0.9), (4096 / 32e3, 4096 / 36e3, 4096 / 40e3)))
     res = {c: [] for c in cands}
     st = stream_handle()
     D, hq, hkv = cfg.head_dim, cfg.heads, cfg.n_kv
@@ -68,7 +69,6 @@ def main():
                 ts.append((e0, e1))
             torch.cuda.synchronize()
             res[c].append(min(x.elapsed_time(y) for x, y in ts) * 1e3)
-    base = (3.0, 1.2, 4096 / 40e3)
     out = sorted(((float(np.mean(v)), c) for c, v in res.items() if v))
     print(f"{len(mixed)} mixed steps; current {base}: {np.mean(res[base]):.1f} us")
     for us, c in out[:10]:

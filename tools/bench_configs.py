@@ -196,13 +196,50 @@ def run_c1(a):
     return out
 
 
+def run_c2u(a):
+    """Unscripted decoding at the C2 shape (SURVEY §8 row f3 at scale): 64
+    requests sample under the native grammar's admissible-token masks
+    (masked greedy picks on the device, random weights) until their token
+    limit; every step reads the picks back (the tracker needs them before
+    the next step), so this is the synchronous serving loop."""
+    cfg = tr.qwen3_8b_shape()
+    model = tr.B200Transformer(cfg)
+    n = 64
+    eng = tr.Engine(model, tr.BatchConfig(max_batch=n, buffer_threshold=2, position_limit=cfg.position_limit,
+                                          pool_pages=n * 1600, max_queue=max(64, n),
+                                          max_output_tokens=a.steps + 8))
+    tools = [tr.ToolSpec("search"), tr.ToolSpec("calc")]
+    for i in range(n):
+        eng.submit(f"q{i}:", tools if i % 2 else [])
+    eng.runtime.precapture()
+    for _ in range(3):
+        eng.step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    toks = steps = 0
+    while not eng.all_terminal():
+        rep = eng.step()
+        toks += sum(rep.decoded.values())
+        steps += 1
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    reqs = list(eng.requests.values())
+    g = next(iter(eng._grammars.values()))
+    return {"config": f"C2 shape, {n} unscripted requests (grammar-masked greedy, half with 2 tools), "
+                      f"max_output_tokens {a.steps + 8}, random weights",
+            "steps": steps, "wall_s": dt, "tokens_per_s": toks / dt, "ms_per_step": 1e3 * dt / max(steps, 1),
+            "statuses": {s: sum(r.status.value == s for r in reqs) for s in ("finished", "failed")},
+            "masks_memoised": {str(k): gg.mask_count for k, gg in eng._grammars.items()},
+            "mean_output_len": sum(r.metrics.output_len for r in reqs) / n}
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", required=True, choices=["c1", "c4", "c5"])
+    ap.add_argument("--config", required=True, choices=["c1", "c2u", "c4", "c5"])
     ap.add_argument("--skip", type=int, default=600)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--prompt", type=int, default=12000, help="C4 prompt tokens")
     ap.add_argument("--requests", type=int, default=32, help="C4 requests")
     ap.add_argument("--complete", action="store_true", help="C4: run every request to completion")
     a = ap.parse_args()
-    print(json.dumps({"c1": run_c1, "c4": run_c4, "c5": run_c5}[a.config](a)))
+    print(json.dumps({"c1": run_c1, "c2u": run_c2u, "c4": run_c4, "c5": run_c5}[a.config](a)))

@@ -38,7 +38,7 @@ def main():
     mixed = [i for i in sorted(timed) if records[i][0].ext][: a.max_mixed]
     resident = rt.replay_upload(records)
     base = (StepDesc.EXT_US_PER_ITEM, StepDesc.EXT_US_PER_QBLOCK_BLOCK, StepDesc.DEC_US_PER_TOKEN)
-    cands = [base, (3.0, 1.2, 4096 / 40e3)] + list(itertools.product((10.0, 12.0, 15.0, 20.0), (0.6, 0.7, 0.8, 0.9), (4096 / 32e3, 4096 / 36e3, 4096 / 40e3)))
+    cands = [base, (3.0, 1.2, 4096 / 40e3)] + list(itertools.product((2.0, 4.0, 6.0, 8.0), (0.6, 0.7, 0.8, 0.9), (4096 / 32e3, 4096 / 36e3, 4096 / 40e3)))
     res = {c: [] for c in cands}
     st = stream_handle()
     D, hq, hkv = cfg.head_dim, cfg.heads, cfg.n_kv

@@ -92,7 +92,10 @@ class Grammar:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            L.load().tim_grammar_destroy(h)
+            try:
+                L.load().tim_grammar_destroy(h)
+            except Exception:      # interpreter shutdown
+                pass
             self._h = None
 
     def tracker(self) -> "Tracker":
@@ -135,7 +138,10 @@ class Tracker:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            L.load().tim_tracker_destroy(h)
+            try:
+                L.load().tim_tracker_destroy(h)
+            except Exception:      # interpreter shutdown
+                pass
             self._h = None
 
     # -------------------------------------------------------------- state

@@ -490,6 +490,9 @@ def gen_masks():
     dump("masks.json.gz", {"vocab": V, "masks": list(distinct), "docs": docs})
 
 
+SCRIPTED: dict = {}
+
+
 def gen_unscripted():
     """Unscripted (grammar-masked greedy) runs of the reference Engine +
     TinyTransformer (fp32, reference weights): per step the report, every
@@ -498,16 +501,23 @@ def gen_unscripted():
     different steps, so each TokenLimit failure frees pages between two other
     requests' allocations (scheduler.py:304-316, 536-548)."""
     scens = []
+    # seed 5 mixes scripted requests (deep(3,2): subtask lists close, prunes
+    # and re-encodes at T=1) with unscripted ones in the same steps
+    SCRIPTED.clear()
+    SCRIPTED[5] = {0: make_trace(deep_recursion_tree(3, 2, seed=0), TOK).script,
+                   2: make_trace(deep_recursion_tree(3, 2, seed=3), TOK).script}
     for seed, prompts, tools, limits, T in [
             (3, ["task:", "q:", "x"], [[], ["search"], []], [60, 200, 130], 1),
             (0, ["task:"], [[]], [150], 0),
-            (1, ["a:", "b:", "c:", "d:"], [[], [], ["calc", "search"], []], [45, 90, 120, 75], 2)]:
+            (1, ["a:", "b:", "c:", "d:"], [[], [], ["calc", "search"], []], [45, 90, 120, 75], 2),
+            (5, ["p:", "u1:", "s:", "u2:"], [[], [], [], []], [400, 70, 400, 110], 1)]:
         m = TinyTransformer(ModelConfig(layers=2, heads=4, head_dim=32, vocab=512, position_limit=512,
                                         seed=seed))
         e = Engine(m, BatchConfig(max_batch=len(prompts), buffer_threshold=T, position_limit=512,
                                   pool_pages=2048, max_output_tokens=400))
-        rids = [e.submit(p, [ToolSpec(n) for n in tl], max_output_tokens=lim)
-                for p, tl, lim in zip(prompts, tools, limits)]
+        scripts = SCRIPTED.get(seed, {})
+        rids = [e.submit(p, [ToolSpec(n) for n in tl], max_output_tokens=lim, script=scripts.get(i))
+                for i, (p, tl, lim) in enumerate(zip(prompts, tools, limits))]
         steps = []
         while not e.all_terminal():
             rep = e.step()
@@ -515,6 +525,7 @@ def gen_unscripted():
                           [crc(e.requests[r].table.pages) for r in rids],
                           [crc(e.requests[r].live) for r in rids], crc(e.pool.free_list)])
         scens.append({"seed": seed, "prompts": prompts, "tools": tools, "limits": limits, "threshold": T,
+                      "scripts": {str(k): v for k, v in scripts.items()},
                       "rids": rids, "steps": steps,
                       "requests": {r: {"logical": e.requests[r].logical, "status": e.requests[r].status.value,
                                        "result": e.result(r), "evictions": [[s.start, s.end] for s in

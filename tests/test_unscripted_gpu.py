@@ -2,8 +2,10 @@
 device must reproduce the REFERENCE Engine + TinyTransformer run bit-exactly.
 
 tests/golden/unscripted_runs.json.gz (oracle/gen_golden.py gen_unscripted) holds
-three reference runs (fp32, reference weights, T = 1 / 0 / 2, tools and no
-tools).  Each request samples under the tracker's admissible-token mask
+four reference runs (fp32, reference weights, T = 1 / 0 / 2 / 1, tools and no
+tools; the fourth mixes two scripted deep(3,2) requests -- subtask lists
+close, prune, re-encode and finish -- with two unscripted ones in the same
+steps).  Each request samples under the tracker's admissible-token mask
 (scheduler.py:413-442, model.py:186-192) until its own max_output_tokens, so
 the TokenLimit failures land on different steps and free their pages between
 other requests' allocations.  The B200 Engine (native grammar tracker, masks
@@ -36,7 +38,7 @@ def _scenarios(golden):
         return json.load(f)
 
 
-@pytest.mark.parametrize("which", [0, 1, 2])
+@pytest.mark.parametrize("which", [0, 1, 2, 3])
 def test_unscripted_masked_greedy_matches_reference(golden, which):
     sc = _scenarios(golden)[which]
     cfg = tr.ModelConfig(layers=2, heads=4, head_dim=32, vocab=512, position_limit=512, seed=sc["seed"])
@@ -44,8 +46,9 @@ def test_unscripted_masked_greedy_matches_reference(golden, which):
                     tr.BatchConfig(max_batch=len(sc["prompts"]), buffer_threshold=sc["threshold"],
                                    position_limit=512, pool_pages=2048, max_output_tokens=400,
                                    check_device=True))
-    rids = [eng.submit(p, [tr.ToolSpec(n) for n in tl], max_output_tokens=lim)
-            for p, tl, lim in zip(sc["prompts"], sc["tools"], sc["limits"])]
+    scripts = {int(k): v for k, v in sc.get("scripts", {}).items()}
+    rids = [eng.submit(p, [tr.ToolSpec(n) for n in tl], max_output_tokens=lim, script=scripts.get(i))
+            for i, (p, tl, lim) in enumerate(zip(sc["prompts"], sc["tools"], sc["limits"]))]
     assert rids == sc["rids"]
     for g in sc["steps"]:
         rep = eng.step()
@@ -59,6 +62,7 @@ def test_unscripted_masked_greedy_matches_reference(golden, which):
         assert eng.requests[r].logical == want["logical"], r
         assert eng.requests[r].status.value == want["status"]
         assert eng.result(r) == want["result"]
+        assert [[x.start, x.end] for x in eng.requests[r].eviction_log] == want["evictions"]
     assert eng.pool.free_count == eng.pool.capacity
 
 

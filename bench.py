@@ -511,6 +511,54 @@ def reference_scripted_rate(budget_s: float, n_req: int, threshold: int):
     return toks / (time.perf_counter() - t0), "reference"
 
 
+def c1_legs() -> dict | None:
+    """SURVEY §8d leg 1 in the same run: BASELINE config 1 (tiny fp32, 2
+    layers x 4 heads x 32, batch 1, deep_recursion_tree(3,2), T=1) through the
+    REFERENCE Engine + TinyTransformer (baseline/_ref, numpy, this host) and
+    through the B200 engine (graphs captured first), same trace; tokens/s of
+    each and whether their text and metrics agree."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "threadrun").is_dir():
+        return None
+    import torch
+    import paper_2507_16784_b200 as tr
+    sys.path.insert(0, str(ref))
+    try:
+        from threadrun import model as rm, scheduler as rs, schema, tokenizer, traces
+    finally:
+        sys.path.remove(str(ref))
+    script = traces.make_trace(schema.deep_recursion_tree(3, 2, seed=0), tokenizer.build_tokenizer()).script
+    kw = dict(layers=2, heads=4, head_dim=32, vocab=512, position_limit=2048)
+    best = None
+    for _ in range(3):
+        e = rs.Engine(rm.TinyTransformer(rm.ModelConfig(**kw)),
+                      rs.BatchConfig(buffer_threshold=1, position_limit=2048, pool_pages=4096))
+        rid = e.submit("p:", script=script)
+        t0 = time.perf_counter()
+        e.run_until_done()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+        rres = e.result(rid)
+    mine = None
+    for _ in range(2):                   # the first pass warms allocator / cuBLAS handles
+        eng = tr.Engine(tr.B200Transformer(tr.ModelConfig(**kw)),
+                        tr.BatchConfig(buffer_threshold=1, position_limit=2048, pool_pages=4096))
+        eng.runtime.precapture()
+        rid2 = eng.submit("p:", script=script)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        while not eng.all_terminal():
+            eng.step()
+        torch.cuda.synchronize()
+        mine = time.perf_counter() - t0
+    res = eng.result(rid2)
+    n = rres["metrics"]["output_len"]
+    return {"workload": "C1 tiny fp32 (2 layers, 4 heads x 32), batch 1, deep_recursion_tree(3,2), T=1",
+            "reference_tokens_per_s": n / best, "reference_kind": "reference (threadrun from baseline/_ref)",
+            "b200_tokens_per_s": res["metrics"]["output_len"] / mine,
+            "identical_text_and_metrics": rres["text"] == res["text"] and rres["metrics"] == res["metrics"]}
+
+
 def scripted_engine_rate(budget_s: float, n_req: int, threshold: int) -> float:
     """SURVEY §8d leg 3: the oracle's reference-order scripted Engine (page
     accounting, no arithmetic) on the C2 requests: host tokens/s."""
@@ -611,6 +659,7 @@ def main():
         cpu = None
         if world == 1 and args.cpu_budget > 0:
             cpu = cpu_reference(args.cpu_budget, args.steps, args.warmup, args.threshold, args.batch)
+            cpu["c1_leg"] = c1_legs()
         value = res["tokens"] / (res["ms"] * 1e-3)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -454,8 +454,10 @@ def gen_masks():
     docs = []
     for r in ev[:40]:
         docs.append({"tools": r["tool_names"], "depth": 16, "stream": r["stream"]})
-    for seed in range(60):
-        tools = [] if seed % 3 == 0 else ["search", "calc"]
+    for seed in range(72):
+        # unusual tool names (multi-byte UTF-8, shared prefixes) in the last 12 walks
+        tools = (["search", "search_web", "calc2", "s"] if seed >= 60 else
+                 ([] if seed % 3 == 0 else ["search", "calc"]))
         depth = (16, 2, 1)[seed % 3 if seed % 5 else 0]
         g = ThreadGrammar([ToolSpec(n) for n in tools], depth, TOK)
         docs.append({"tools": tools, "depth": depth,

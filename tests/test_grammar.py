@@ -3,8 +3,9 @@ against the REFERENCE tracker's own outputs (CPU, host code only):
 
 * lifecycle events of the 157 golden documents (tracker.py Tracker.feed,
   tests/golden/events.json.gz), offsets / depths / payloads bit-exact;
-* allowed_mask at EVERY position of 100 documents (40 golden streams, 60
-  reference random_mask_walk documents under tools / no tools and depth limits
+* allowed_mask at EVERY position of 112 documents (40 golden streams, 72
+  reference random_mask_walk documents under tools / no tools (incl. prefix-sharing
+  tool names s / search / search_web) and depth limits
   16 / 2 / 1), tests/golden/masks.json.gz;
 * the Rejected message (byte index and context) for inadmissible tokens.
 """
